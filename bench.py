@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""Benchmark of the register-cache stencil hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME]
+                    [--variant shuffle|plain] [--impl ours|reference]
+
+One *step* = one ``stencil_run(n_iters)`` of the workload (Dirichlet ring
+copy + n_iters sweeps, one CUDA graph), i.e. one pass of the whole hot path
+(DESIGN.md §1 rows S1-S9) over one synthetic grid.  Default workload:
+BASELINE.json configs[1], gaussblur 5x5 fp32 8192x8192, 100 iterations;
+for N>1 weak-scaled to 8192 x (8192*N) with a y-slab decomposition and NCCL
+halo exchange.  Prints ONE JSON line (rank 0).
+
+Metric (BASELINE.json): Gpoints/s (interior points x sweeps / s, all ranks)
+and achieved HBM GB/s as a fraction of the measured copy bandwidth.
+
+--impl reference: the CPU oracle (oracle/, the plain fp64 C loop nests)
+timed on this host's cores on a bounded sample of the same workload; this
+is the only other place bench.py executes oracle/ (besides cpu_baseline).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# name -> kind, dtype, dims at N=1 (x fastest), iterations, weak-scaled axis
+WORKLOADS = {
+    "gaussblur": dict(kind="gaussblur5x5", dtype="f32", dims=(8192, 8192), iters=100,
+                      config="BASELINE configs[1]: gaussblur 5x5 fp32 8192x8192, 100 iterations"),
+    "jacobi2d": dict(kind="jacobi2d5", dtype="f32", dims=(512, 512), iters=10,
+                     config="BASELINE configs[0]: jacobi 2D 5-point fp32 512x512, 10 sweeps"),
+    "jacobi2d_paper": dict(kind="jacobi2d5", dtype="f32", dims=(32768, 32768), iters=10,
+                           config="jacobi 2D 5-point fp32 at the paper's 2-D size 32768^2 (PAPER.md:644)"),
+    "gameoflife": dict(kind="gameoflife", dtype="i32", dims=(16384, 16384), iters=10,
+                       config="BASELINE configs[3]: gameoflife int32 16384x16384"),
+    "laplacian": dict(kind="laplacian3d7", dtype="f64", dims=(512, 512, 512), iters=10,
+                      config="BASELINE configs[2]: laplacian 3D 7-point fp64 512^3"),
+    "wave13pt": dict(kind="wave13pt", dtype="f64", dims=(512, 512, 512), iters=10,
+                     config="BASELINE configs[2]: wave13pt 3D 13-point fp64 512^3"),
+    "tricubic": dict(kind="tricubic", dtype="f32", dims=(256, 256, 256), iters=10,
+                     config="BASELINE configs[3]: tricubic 3D fp32 256^3"),
+    "jacobi3d": dict(kind="jacobi3d7", dtype="f32", dims=(1024, 1024, 1024), iters=10,
+                     config="BASELINE configs[4]: jacobi 3D 7-point fp32 1024^2 x (1024*N)"),
+    "divergence": dict(kind="divergence", dtype="f32", dims=(512, 512, 512), iters=10,
+                       config="divergence fp32 512^3 (suite member, Table 1)"),
+    "gradient": dict(kind="gradient", dtype="f32", dims=(512, 512, 512), iters=10,
+                     config="gradient fp32 512^3 (suite member, Table 1)"),
+}
+L2_BYTES = 126 * 2**20
+METRIC = "Gpoints/s and achieved HBM GB/s (% of ~8 TB/s) per stencil, 1/2/4/8 B200"
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def profile_traffic(workload, variant):
+    """dram bytes per launch from a committed ncu --set full summary, or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(f"{workload}:{variant}")
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------- oracle (CPU)
+def oracle_sample(wl, seconds: float, nthreads: int):
+    """Time the CPU oracle, as it stands, on a bounded crop of the workload.
+
+    Runs whole sweeps of the oracle on a crop (same generator, same kind,
+    dtype and iteration structure) until `seconds` of wall time pass.
+    Returns (Gpoints/s, description)."""
+    import numpy as np
+    from oracle import pyoracle
+    from paper_2301_11389_b200 import inputs
+
+    kind, dt = wl["kind"], wl["dtype"]
+    ar = pyoracle.arity(kind)
+    if len(wl["dims"]) == 2:
+        crop = (min(wl["dims"][1], 2048), min(wl["dims"][0], 2048))
+    else:
+        crop = tuple(min(d, 128) for d in wl["dims"][::-1])
+    seed = inputs.BASE_SEED
+    fields = [inputs.generate_np(crop, dt, seed, a) for a in range(max(ar["n_in"], 1))]
+    if ar["n_bufs"] == 2:
+        bufs = [fields[0], np.zeros_like(fields[0])]
+    elif kind == "wave13pt":
+        bufs = [fields[0], fields[1], np.zeros_like(fields[0])]
+    else:
+        bufs = fields[: ar["n_in"]] + [np.zeros_like(fields[0]) for _ in range(ar["n_out"])]
+    interior = 1
+    for n in crop:
+        interior *= n - ar["lo"] - ar["hi"]
+    sweeps, t0 = 0, time.perf_counter()
+    while True:
+        pyoracle.run(kind, dt, bufs, 1, nthreads=nthreads)
+        sweeps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return interior * sweeps / el / 1e9, (f"{kind} {dt} crop {'x'.join(map(str, crop[::-1]))}, "
+                                          f"{sweeps} sweeps in {el:.1f} s, {nthreads} threads")
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------ reference
+def run_reference(args, wl, world, rank):
+    if rank != 0:
+        return
+    cores = host_cores()
+    per_step = max(2.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(wl, per_step / 4, cores)
+    vals, descs = [], []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, d = oracle_sample(wl, per_step, cores)
+        vals.append(v)
+        descs.append(d)
+    el = time.perf_counter() - t0
+    value = sum(vals) / len(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Gpoints/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": wl["dtype"], "data": "synthetic (splitmix64, DESIGN.md §6)",
+        "config": {"workload": wl["config"], "kind": wl["kind"], "dims": list(wl["dims"]),
+                   "iters": wl["iters"]},
+        "cpu_baseline": {"value": value, "unit": "Gpoints/s", "cores": cores, "kind": "oracle",
+                         "sample": descs[-1]},
+        "e2e": {"value": value, "unit": "Gpoints/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ ours
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="gaussblur", choices=sorted(WORKLOADS))
+    ap.add_argument("--variant", default="shuffle", choices=["shuffle", "plain"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    wl = dict(WORKLOADS[args.workload])
+
+    if args.impl == "reference":
+        run_reference(args, wl, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2301_11389_b200 import build, inputs
+    from paper_2301_11389_b200.binding import Stencil, dist_get_id
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    build.build()                     # no-op when the in-tree .so is current
+
+    dims = list(wl["dims"])
+    dims[-1] *= world                 # weak scaling along the slowest axis
+    st = Stencil(wl["kind"], dims, wl["dtype"], variant=args.variant)
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(dist_get_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        st.attach(bytes(uid.cpu().tolist()), rank, world)
+    info = st.info()
+    n_in, n_out, n_bufs = st.arity()
+    ldims = info["local_dims"][: len(dims)]
+    shape = tuple(ldims[::-1])
+    # synthetic inputs generated on the device (same counter-based recipe as
+    # the host generator: tests/test_inputs_gpu.py checks bit equality)
+    seed = inputs.BASE_SEED + 1
+    fields = [inputs.generate_torch(shape, wl["dtype"], seed + 97 * rank, a) for a in range(n_in)]
+    if n_bufs == 2:
+        bufs = [fields[0], torch.zeros_like(fields[0])]
+    elif wl["kind"] == "wave13pt":
+        bufs = [fields[0], fields[1], torch.zeros_like(fields[0])]
+    else:
+        bufs = fields + [torch.zeros_like(fields[0]) for _ in range(n_out)]
+    nbytes_buf = bufs[0].numel() * bufs[0].element_size()
+    flush = None
+    if nbytes_buf * len(bufs) < 2 * L2_BYTES:
+        flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    iters = wl["iters"]
+
+    def step():
+        return st.run(bufs, iters, stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, events on the launching stream
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for a, b in evs:
+            if flush is not None:
+                flush.fill_(1.0)          # evict the grid from L2 between timed steps
+            a.record(stream)
+            step()
+            b.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    pts_rank = info["interior_points"]
+    pts_all = torch.tensor([float(pts_rank)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(pts_all)
+    pts_all = float(pts_all.item())
+    value = pts_all * iters * args.steps / (ms / 1e3) / 1e9
+    clocks = clk.summary()
+
+    # ---- roofline of the dominant kernel (the sweep kernel)
+    launches = iters * info["launches_per_step"]
+    avg_launch_s = ms / 1e3 / (args.steps * iters)            # includes graph gaps: conservative
+    alg_bytes = info["bytes_per_point"] * pts_rank              # per sweep on this rank
+    achieved = alg_bytes / avg_launch_s / 1e9
+    peak, peak_src = measured_peaks()
+    traffic = profile_traffic(args.workload, args.variant)
+
+    # kernel-only timing: individual stencil_step launches bracketed by events
+    k_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(6)]
+    ins = bufs[:n_in] if n_bufs != 2 else [bufs[0]]
+    outs = bufs[n_in:] if n_bufs not in (2, 3) else [bufs[-1] if n_bufs == 3 else bufs[1]]
+    if wl["kind"] == "wave13pt":
+        ins, outs = [bufs[0], bufs[1]], [bufs[2]]
+    for a, b in k_ev:
+        if flush is not None:
+            flush.fill_(1.0)
+        a.record(stream)
+        st.step(ins, outs, stream)
+        b.record(stream)
+    torch.cuda.synchronize()
+    k_ms = sorted(a.elapsed_time(b) for a, b in k_ev[1:])
+    k_med = k_ms[len(k_ms) // 2]
+
+    # ---- end to end through the C ABI with HOST buffers
+    e2e = None
+    if not args.no_e2e:
+        n_up = 1 if n_bufs == 2 else (2 if wl["kind"] == "wave13pt" else n_in)
+        n_down = 1 if n_bufs in (2, 3) else n_out
+        h_in = [bufs[a].cpu().pin_memory() for a in range(n_up)]
+        h_out = [torch.empty_like(h_in[0]).pin_memory() for _ in range(n_down)]
+        st.run_host(h_in, h_out, bufs, iters, stream)       # warm-up
+        e_ms = []
+        for _ in range(max(2, min(args.steps, 3))):
+            if world > 1:
+                dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            st.run_host(h_in, h_out, bufs, iters, stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            e_ms.append(a.elapsed_time(b))
+        et = torch.tensor([sum(e_ms) / len(e_ms)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": pts_all * iters / (float(et.item()) / 1e3) / 1e9, "unit": "Gpoints/s",
+               "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() for x in h_in)),
+               "d2h_bytes_per_step": int(sum(x.numel() * x.element_size() for x in h_out))}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = host_cores()
+        v, desc = oracle_sample(wl, args.cpu_seconds, cores)
+        cpu = {"value": v, "unit": "Gpoints/s", "cores": cores, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gpoints/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": wl["dtype"], "data": "synthetic (splitmix64 seeded grids, DESIGN.md §6)",
+            "config": {"workload": wl["config"], "kind": wl["kind"], "dims": dims,
+                       "local_dims": list(ldims), "iters_per_step": iters,
+                       "variant": args.variant, "parallelism": f"slab{world}" if world > 1 else "1gpu",
+                       "l2": "flushed between timed steps" if flush is not None
+                       else "inputs larger than L2"},
+            "hbm_gbs": achieved * 1.0,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "alg_bytes_per_launch": alg_bytes, "avg_launch_us": avg_launch_s * 1e6,
+                         "kernel_only_us": k_med * 1e3,
+                         "kernel_only_frac": alg_bytes / (k_med / 1e3) / 1e9 / peak},
+            "clocks": clocks,
+            "e2e": e2e,
+            "gpu_launches": args.steps * (launches + (2 if wl["kind"] == "wave13pt" else
+                                                       (1 if n_bufs == 2 else 0))),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    st.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

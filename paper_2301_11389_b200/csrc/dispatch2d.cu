@@ -1,0 +1,80 @@
+// dispatch2d.cu — host launchers of the 2-D kernels (k2d.cuh).
+#include "internal.h"
+#include "k2d.cuh"
+
+namespace stb200 {
+
+static int sm_count(int device) {
+    static int cached[64] = {0};
+    if (device < 0 || device >= 64) return 148;
+    if (!cached[device]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+        cached[device] = n > 0 ? n : 148;
+    }
+    return cached[device];
+}
+
+// Strip height: enough strips that the grid is one full wave of resident CTAs
+// (grid sized in multiples of the SM count), but never shorter than kMinH rows
+// so the 2R re-read rows per strip stay a small fraction.
+template <class Op, typename T, int VAR>
+static cudaError_t launch_k2d(const stencil_s* h, const void* in, void* out, cudaStream_t s,
+                              int64_t y_lo, int64_t y_hi) {
+    constexpr int R = Op::R;
+    constexpr int V = vlen<T>();
+    constexpr int kMinH = 16;
+    auto kern = k2d<Op, T, VAR>;
+    static int blocks_per_sm = 0;
+    if (!blocks_per_sm) {
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern,
+                                                                      kWarps2D * 32, 0);
+        if (e != cudaSuccess || blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    const int64_t nx = h->ldims[0], ny = h->ldims[1];
+    if (y_lo < 0) { y_lo = R; y_hi = ny - R; }
+    if (y_hi <= y_lo) return cudaSuccess;
+    const int64_t ntiles = (nx + 32 * V - 1) / (32 * V);
+    const int64_t gx = (ntiles + kWarps2D - 1) / kWarps2D;
+    const int64_t slots = (int64_t)blocks_per_sm * sm_count(h->device);
+    const int64_t rows = y_hi - y_lo;
+    int64_t nstrips = slots / gx;
+    if (nstrips < 1) nstrips = 1;
+    int64_t H = (rows + nstrips - 1) / nstrips;
+    if (H < kMinH) H = kMinH;
+    nstrips = (rows + H - 1) / H;
+    Coeffs<T, Op::NC> c{};
+    for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)h->coeffs[t];
+    kern<<<dim3((unsigned)gx, (unsigned)nstrips), kWarps2D * 32, 0, s>>>(
+        (const T*)in, (T*)out, nx, (int)y_lo, (int)y_hi, (int)H, c);
+    return cudaGetLastError();
+}
+
+template <template <typename> class OpT, typename T>
+static cudaError_t launch_var(const stencil_s* h, const void* in, void* out, cudaStream_t s,
+                              int64_t a, int64_t b) {
+    if (h->variant == ST_PLAIN) return launch_k2d<OpT<T>, T, VAR_PLAIN>(h, in, out, s, a, b);
+    return launch_k2d<OpT<T>, T, VAR_SHUFFLE>(h, in, out, s, a, b);
+}
+
+cudaError_t dispatch_2d(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
+                        int64_t a, int64_t b) {
+    const bool f64 = h->dtype == ST_F64;
+    switch (h->k->kind) {
+    case ST_JACOBI2D5:
+        return f64 ? launch_var<OpJacobi2D5, double>(h, in[0], out[0], s, a, b)
+                   : launch_var<OpJacobi2D5, float>(h, in[0], out[0], s, a, b);
+    case ST_JACOBI2D9:
+        return f64 ? launch_var<OpJacobi2D9, double>(h, in[0], out[0], s, a, b)
+                   : launch_var<OpJacobi2D9, float>(h, in[0], out[0], s, a, b);
+    case ST_GAUSSBLUR5X5:
+        return f64 ? launch_var<OpGauss5, double>(h, in[0], out[0], s, a, b)
+                   : launch_var<OpGauss5, float>(h, in[0], out[0], s, a, b);
+    case ST_GAMEOFLIFE:
+        if (h->variant == ST_PLAIN) return launch_k2d<OpLife, int, VAR_PLAIN>(h, in[0], out[0], s, a, b);
+        return launch_k2d<OpLife, int, VAR_SHUFFLE>(h, in[0], out[0], s, a, b);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace stb200

@@ -1,0 +1,261 @@
+// dist.cu — 1-D slab decomposition along the slowest axis with NCCL halo
+// exchange over NVLink / NVSwitch, one process per GPU.
+//
+// Not in the paper (single GPU): the decomposition named by
+// BASELINE.json north_star.  Layout: the global slow extent n (boundary
+// planes included) is split into N slabs of m = n/N planes; every rank's
+// local buffers hold lo + m + hi planes, local plane L <-> global plane
+// p*m - lo + L.  Rank 0's first lo and rank N-1's last hi local planes lie
+// outside the domain and are never read.
+//
+// One step (stencil_step) on rank p:
+//   s:    record e_in                         (inputs of this step complete)
+//   comm: wait e_in; ncclGroupStart;
+//           send local [lo, lo+hi)  -> p-1;  recv local [0, lo)        <- p-1
+//           send local [m, m+lo)    -> p+1;  recv local [lo+m, lo+m+hi) <- p+1
+//         ncclGroupEnd; record e_comm
+//   s:    interior kernel over the output planes that read no halo plane
+//         (overlaps the exchange), wait e_comm, then the (at most two) thin
+//         slabs of output planes that read a halo plane.
+// Results are bit-identical to one GPU: per-point arithmetic is unchanged.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "internal.h"
+
+// Minimal NCCL ABI subset (nccl.h, NCCL 2.x; stable since 2.0).
+typedef struct ncclComm* ncclComm_t;
+typedef int ncclResult_t;                       // ncclSuccess = 0
+typedef struct { char internal[128]; } ncclUniqueId;
+static const int kNcclInt8 = 0;                 // ncclInt8 == ncclChar
+
+namespace stb200 {
+
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+// The process's libnccl.so.2 (the one torch already loaded, if any: dlopen
+// returns the resident copy, so only one NCCL lives in the process).
+static NcclApi& nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* so = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!so) so = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (so) {
+#define LOAD(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(so, "nccl" #f))
+            LOAD(GetUniqueId); LOAD(CommInitRank); LOAD(CommDestroy); LOAD(Send); LOAD(Recv);
+            LOAD(GroupStart); LOAD(GroupEnd); LOAD(GetErrorString);
+#undef LOAD
+            api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send &&
+                     api.Recv && api.GroupStart && api.GroupEnd && api.GetErrorString;
+        }
+    }
+    return api;
+}
+
+struct DistState {
+    ncclComm_t comm = nullptr;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t e_in = nullptr, e_comm = nullptr;
+    int64_t n = 0, m = 0;            // global slow extent, planes per rank
+    int64_t plan[8] = {0};
+    size_t plane_bytes = 0;
+};
+
+// Inputs with taps along the slow axis (their halo planes must be exchanged).
+static unsigned halo_inputs(int kind) {
+    switch (kind) {
+    case ST_WAVE13PT: return 1u << 1;      // cur; prev is read at the centre only
+    case ST_DIVERGENCE: return 1u << 2;    // w carries the z taps
+    default: return 1u;                    // the single field / u / f
+    }
+}
+
+int64_t dist_owned_interior_points(const stencil_s* h) {
+    const DistState* d = h->dist;
+    const int lo = h->k->lo, hi = h->k->hi;
+    const int64_t ga = std::max<int64_t>((int64_t)h->rank * d->m, lo);
+    const int64_t gb = std::min<int64_t>((int64_t)(h->rank + 1) * d->m, d->n - hi);
+    int64_t planes = gb > ga ? gb - ga : 0;
+    int64_t per = h->ldims[0] - lo - hi;
+    if (h->ndims == 3) per *= h->ldims[1] - lo - hi;
+    return planes * per;
+}
+
+// Output slabs of this rank in local planes: [a, b) owned interior, split into
+// lower halo-dependent [a, x0), independent [x0, x1), upper dependent [x1, b).
+static void output_slabs(const stencil_s* h, int64_t* a, int64_t* x0, int64_t* x1, int64_t* b) {
+    const DistState* d = h->dist;
+    const int lo = h->k->lo, hi = h->k->hi;
+    const int64_t base = (int64_t)h->rank * d->m;
+    const int64_t ga = std::max<int64_t>(base, lo), gb = std::min<int64_t>(base + d->m, d->n - hi);
+    *a = ga - base + lo;
+    *b = gb - base + lo;
+    if (*b < *a) *b = *a;
+    const bool has_lower = h->rank > 0, has_upper = h->rank < h->nranks - 1;
+    int64_t dep_lo_end = has_lower ? 2 * lo : *a;          // outputs < 2lo read planes < lo
+    int64_t dep_hi_begin = has_upper ? lo + d->m - hi : *b; // outputs >= lo+m-hi read >= lo+m
+    *x0 = std::min(std::max(*a, dep_lo_end), *b);
+    *x1 = std::max(std::min(*b, dep_hi_begin), *x0);
+}
+
+int dist_launches_per_step(const stencil_s* h) {
+    int64_t a, x0, x1, b;
+    output_slabs(h, &a, &x0, &x1, &b);
+    return (x0 > a) + (x1 > x0) + (b > x1);
+}
+
+static int nccl_check(ncclResult_t r, const char* what) {
+    if (r == 0) return ST_OK;
+    return set_error(ST_ENCCL, "%s: %s", what, nccl().GetErrorString(r));
+}
+
+int dist_step(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s) {
+    DistState* d = h->dist;
+    NcclApi& api = nccl();
+    const int lo = h->k->lo, hi = h->k->hi;
+    const int64_t m = d->m;
+    const size_t pb = d->plane_bytes;
+    const bool has_lower = h->rank > 0, has_upper = h->rank < h->nranks - 1;
+    cudaError_t e;
+
+    // 1. exchange the halo planes of every input with slow-axis taps
+    if ((e = cudaEventRecord(d->e_in, s)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(d->comm_stream, d->e_in, 0)) != cudaSuccess)
+        return set_error(ST_ECUDA, "event: %s", cudaGetErrorString(e));
+    int rc;
+    if ((rc = nccl_check(api.GroupStart(), "ncclGroupStart"))) return rc;
+    const unsigned mask = halo_inputs(h->k->kind);
+    for (int a = 0; a < h->k->n_in; ++a) {
+        if (!(mask >> a & 1u)) continue;
+        char* buf = (char*)in[a];      // the halo planes of an input are the exchange's
+        if (has_lower) {
+            api.Send(buf + (size_t)lo * pb, (size_t)hi * pb, kNcclInt8, h->rank - 1, d->comm, d->comm_stream);
+            api.Recv(buf, (size_t)lo * pb, kNcclInt8, h->rank - 1, d->comm, d->comm_stream);
+        }
+        if (has_upper) {
+            api.Send(buf + (size_t)m * pb, (size_t)lo * pb, kNcclInt8, h->rank + 1, d->comm, d->comm_stream);
+            api.Recv(buf + (size_t)(lo + m) * pb, (size_t)hi * pb, kNcclInt8, h->rank + 1, d->comm,
+                     d->comm_stream);
+        }
+    }
+    if ((rc = nccl_check(api.GroupEnd(), "ncclGroupEnd"))) return rc;
+    if ((e = cudaEventRecord(d->e_comm, d->comm_stream)) != cudaSuccess)
+        return set_error(ST_ECUDA, "event: %s", cudaGetErrorString(e));
+
+    // 2. interior planes (overlap the exchange), 3. halo-dependent slabs
+    int64_t a, x0, x1, b;
+    output_slabs(h, &a, &x0, &x1, &b);
+    if (x1 > x0 && (rc = launch_sweep(h, in, out, s, x0, x1))) return rc;
+    if ((e = cudaStreamWaitEvent(s, d->e_comm, 0)) != cudaSuccess)
+        return set_error(ST_ECUDA, "event wait: %s", cudaGetErrorString(e));
+    if (x0 > a && (rc = launch_sweep(h, in, out, s, a, x0))) return rc;
+    if (b > x1 && (rc = launch_sweep(h, in, out, s, x1, b))) return rc;
+    return ST_OK;
+}
+
+void dist_release(stencil_s* h) {
+    DistState* d = h->dist;
+    if (!d) return;
+    if (d->comm && nccl().ok) nccl().CommDestroy(d->comm);
+    if (d->e_in) cudaEventDestroy(d->e_in);
+    if (d->e_comm) cudaEventDestroy(d->e_comm);
+    if (d->comm_stream) cudaStreamDestroy(d->comm_stream);
+    delete d;
+    h->dist = nullptr;
+}
+
+// Full-plane ranges of the Dirichlet ring copy in local slow-axis planes.
+void dist_ring_planes(const stencil_s* h, int64_t* full_lo, int64_t* full_hi) {
+    const int lo = h->k->lo, hi = h->k->hi;
+    const int64_t m = h->dist->m;
+    *full_lo = h->rank == 0 ? 2 * lo : 0;                        // dead + boundary planes
+    *full_hi = h->rank == h->nranks - 1 ? lo + m - hi : lo + m + hi;
+}
+
+}  // namespace stb200
+
+using namespace stb200;
+
+extern "C" int stencil_slab_plan(int64_t n, int lo, int hi, int rank, int nranks, int64_t plan[8]) {
+    if (!plan) return set_error(ST_EARG, "null plan");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(ST_EARG, "bad rank/nranks");
+    if (lo < 0 || hi < 0 || lo > 0xFFFF || hi > 0xFFFF) return set_error(ST_EARG, "bad halo");
+    if (n % nranks) return set_error(ST_EARG, "slow extent %lld not divisible by %d", (long long)n, nranks);
+    const int64_t m = n / nranks;
+    if (m < lo || m < hi || m < 1) return set_error(ST_EARG, "slab of %lld planes thinner than the halo", (long long)m);
+    plan[0] = (int64_t)rank * m;                    // own_begin (global)
+    plan[1] = (int64_t)(rank + 1) * m;              // own_end (global)
+    plan[2] = m + lo + hi;                          // local planes
+    plan[3] = rank > 0 ? 0 : -1;                    // recv_lo_at   (lo planes from rank-1)
+    plan[4] = rank > 0 ? lo : -1;                   // send_lo_from (hi planes to rank-1)
+    plan[5] = rank < nranks - 1 ? lo + m : -1;      // recv_hi_at   (hi planes from rank+1)
+    plan[6] = rank < nranks - 1 ? m : -1;           // send_hi_from (lo planes to rank+1)
+    plan[7] = (int64_t)lo | ((int64_t)hi << 16);
+    return ST_OK;
+}
+
+extern "C" int stencil_dist_get_id(uint8_t id[128]) {
+    if (!id) return set_error(ST_EARG, "null id");
+    NcclApi& api = nccl();
+    if (!api.ok) return set_error(ST_ENCCL, "libnccl.so.2 not loadable: %s", dlerror());
+    ncclUniqueId u;
+    int rc = nccl_check(api.GetUniqueId(&u), "ncclGetUniqueId");
+    if (rc) return rc;
+    memcpy(id, u.internal, 128);
+    return ST_OK;
+}
+
+extern "C" int stencil_dist_attach(stencil_t h, const uint8_t id[128], int rank, int nranks) {
+    if (!h || !id) return set_error(ST_EARG, "null argument");
+    if (h->dist) return set_error(ST_ESTATE, "handle already attached");
+    if (!h->graphs.empty()) return set_error(ST_ESTATE, "attach before the first run");
+    const int slow = h->ndims - 1;
+    int64_t plan[8];
+    int rc = stencil_slab_plan(h->dims[slow], h->k->lo, h->k->hi, rank, nranks, plan);
+    if (rc) return rc;
+    NcclApi& api = nccl();
+    if (!api.ok) return set_error(ST_ENCCL, "libnccl.so.2 not loadable");
+    cudaSetDevice(h->device);
+    DistState* d = new DistState();
+    d->n = h->dims[slow];
+    d->m = d->n / nranks;
+    memcpy(d->plan, plan, sizeof plan);
+    const size_t es = h->dtype == ST_F64 ? 8 : 4;
+    d->plane_bytes = (size_t)h->dims[0] * (h->ndims == 3 ? (size_t)h->dims[1] : 1) * es;
+    cudaError_t e;
+    if ((e = cudaStreamCreateWithFlags(&d->comm_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&d->e_in, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&d->e_comm, cudaEventDisableTiming)) != cudaSuccess) {
+        h->dist = d;
+        dist_release(h);
+        return set_error(ST_ECUDA, "attach: %s", cudaGetErrorString(e));
+    }
+    ncclUniqueId u;
+    memcpy(u.internal, id, 128);
+    rc = nccl_check(api.CommInitRank(&d->comm, nranks, u, rank), "ncclCommInitRank");
+    if (rc) {
+        d->comm = nullptr;
+        h->dist = d;
+        dist_release(h);
+        return rc;
+    }
+    h->dist = d;
+    h->rank = rank;
+    h->nranks = nranks;
+    h->ldims[slow] = plan[2];
+    return ST_OK;
+}

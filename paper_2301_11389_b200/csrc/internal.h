@@ -1,0 +1,67 @@
+// internal.h — handle layout and cross-file declarations of libstencil_b200
+// (not part of the C ABI).
+#pragma once
+#include <cstdarg>
+#include <cstdint>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/stencil.h"
+
+namespace stb200 {
+
+struct KindInfo {
+    int kind;
+    const char* name;
+    int ndims, n_in, n_out, lo, hi, ncoeffs;
+    int iterable;          // 1 ping-pong, 2 three-level (wave13pt), 0 re-apply
+    bool allow_f, allow_i;
+};
+
+struct GraphEntry {
+    void* bufs[8];
+    int nb, n_iters, variant, result;
+    cudaGraphExec_t exec;
+};
+
+struct DistState;          // dist.cu
+
+}  // namespace stb200
+
+struct stencil_s {
+    const stb200::KindInfo* k = nullptr;
+    int dtype = 0, ndims = 0, variant = 0, device = 0;
+    int64_t dims[3] = {1, 1, 1};     // global
+    int64_t ldims[3] = {1, 1, 1};    // local buffers (slab + halo when attached)
+    double coeffs[32] = {0};
+    cudaStream_t cap = nullptr;      // graph-capture stream
+    std::vector<stb200::GraphEntry> graphs;
+    std::vector<int> tmaps;          // reserved
+    // multi-GPU
+    stb200::DistState* dist = nullptr;
+    int rank = 0, nranks = 1;
+};
+
+namespace stb200 {
+
+int set_error(int code, const char* fmt, ...);
+const KindInfo* kind_info(int kind);
+int64_t interior_points(const stencil_s* h);
+
+// Launch the kernel of h for output slow-axis range [s_begin, s_end) of the
+// local buffers (-1,-1 = the whole interior).  dispatch.cu.
+cudaError_t dispatch_kernel(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
+                            int64_t s_begin, int64_t s_end);
+int launch_sweep(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
+                 int64_t s_begin, int64_t s_end);
+int ring_copy(const stencil_s* h, const void* src, void* dst, cudaStream_t s);
+
+// dist.cu
+int dist_step(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s);
+void dist_release(stencil_s* h);
+int64_t dist_owned_interior_points(const stencil_s* h);
+int dist_launches_per_step(const stencil_s* h);
+void dist_ring_planes(const stencil_s* h, int64_t* full_lo, int64_t* full_hi);
+
+}  // namespace stb200

@@ -1,0 +1,140 @@
+"""GPU parity of the 2-D kernels against the CPU oracle (through the C ABI).
+
+Sizes the oracle finishes in seconds that span several warp tiles (128 fp32 /
+64 fp64 columns), several CTAs (4 tiles) and ragged tails in x and y; the
+minimum grids (one interior point along an axis); SHUFFLE vs PLAIN
+bit-identity; and the BASELINE configs at full size (jacobi 512^2 x 10 whole
+grid; gaussblur 8192^2 x 100 and gameoflife 16384^2 x 10 on dependence-cone
+windows, in the launch configuration bench.py times).
+"""
+import zlib
+
+import numpy as np
+import pytest
+
+from paper_2301_11389_b200 import inputs
+from parity import (assert_parity, gpu_run, gpu_step, interior, oracle_window_run, ring_mask)
+
+pytestmark = pytest.mark.gpu
+
+KINDS_2D = [("jacobi2d5", 1), ("jacobi2d9", 1), ("gaussblur5x5", 2), ("gameoflife", 1)]
+SHAPES = {  # (ny, nx): numpy order.  nx*sizeof(T) % 16 == 0 (the ABI's vector rule)
+    4: [(3, 4), (5, 8), (29, 36), (61, 132), (33, 516), (130, 260), (77, 1028), (9, 2052)],
+    8: [(3, 4), (5, 6), (29, 34), (61, 66), (45, 130), (33, 258), (19, 1026)],
+}
+
+
+def dtypes_for(kind):
+    return ["i32"] if kind == "gameoflife" else ["f32", "f64"]
+
+
+def cases():
+    for kind, r in KINDS_2D:
+        for dt in dtypes_for(kind):
+            for shape in SHAPES[8 if dt == "f64" else 4]:
+                if min(shape) >= 2 * r + 1:
+                    yield kind, dt, shape
+
+
+@pytest.mark.parametrize("kind,dtype,shape", list(cases()),
+                         ids=lambda v: v if isinstance(v, str) else "x".join(map(str, v)))
+def test_step_parity_and_variants(oracle, kind, dtype, shape):
+    seed = inputs.BASE_SEED + zlib.crc32(repr((kind, dtype, shape)).encode()) % 1000
+    f = inputs.generate_np(shape, dtype, seed)
+    ar = oracle.arity(kind)
+    ref = np.full_like(f, 0)
+    oracle.step(kind, dtype, [f], [ref])
+    outs = {}
+    for var in ("shuffle", "plain"):
+        (g,) = gpu_step(kind, dtype, [f], 1, variant=var, fill=0)
+        sl = interior(shape, ar["lo"], ar["hi"])
+        assert_parity(g[sl], ref[sl], dtype, f"{kind} {dtype} {shape} {var}")
+        assert np.all(g[ring_mask(shape, ar["lo"], ar["hi"])] == 0), "boundary ring written"
+        outs[var] = g
+    assert np.array_equal(outs["shuffle"].view(np.uint8), outs["plain"].view(np.uint8)), \
+        "SHUFFLE and PLAIN differ"
+
+
+@pytest.mark.parametrize("kind,dtype,shape", [
+    ("jacobi2d5", "f32", (61, 132)), ("jacobi2d9", "f64", (45, 130)),
+    ("gaussblur5x5", "f32", (77, 1028)), ("gaussblur5x5", "f64", (33, 258)),
+    ("gameoflife", "i32", (130, 260))])
+def test_run_parity(oracle, kind, dtype, shape):
+    f = inputs.generate_np(shape, dtype, inputs.BASE_SEED + 7)
+    bufs = [f.copy(), np.zeros_like(f)]
+    ridx = oracle.run(kind, dtype, bufs, 7)
+    for var in ("shuffle", "plain"):
+        gidx, gb = gpu_run(kind, dtype, [f.copy(), np.full_like(f, 9)], 7, variant=var)
+        assert gidx == ridx
+        assert_parity(gb[gidx], bufs[ridx], dtype, f"{kind} run {var}")
+        # Dirichlet ring copied into the other buffer, untouched in the result
+        ar = oracle.arity(kind)
+        m = ring_mask(shape, ar["lo"], ar["hi"])
+        assert np.array_equal(gb[1 - gidx][m], f[m]) and np.array_equal(gb[gidx][m], f[m])
+
+
+def test_user_coefficients(oracle):
+    shape = (40, 264)
+    f = inputs.generate_np(shape, "f32", 3)
+    w = np.linspace(-1, 1, 25)
+    ref = np.zeros_like(f)
+    oracle.step("gaussblur5x5", "f32", [f], [ref], coeffs=w)
+    (g,) = gpu_step("gaussblur5x5", "f32", [f], 1, coeffs=w)
+    assert_parity(g[2:-2, 2:-2], ref[2:-2, 2:-2], "f32", "gaussblur custom weights")
+
+
+def test_closed_form_on_gpu(oracle):
+    """Pins re-run on the GPU: i^2+j^2 -> +1 under the 5-point Jacobi."""
+    j, i = np.meshgrid(np.arange(200.0), np.arange(256.0), indexing="ij")
+    f = (i * i + j * j).astype(np.float32)
+    (g,) = gpu_step("jacobi2d5", "f32", [f], 1)
+    np.testing.assert_array_equal(g[1:-1, 1:-1], f[1:-1, 1:-1] + 1)
+
+
+def test_life_glider_on_gpu():
+    g = np.zeros((40, 260), np.int32)
+    for r, c in [(1, 2), (2, 3), (3, 1), (3, 2), (3, 3)]:
+        g[r, c + 125] = 1            # crosses the warp-tile boundary at column 128
+    idx, res = gpu_run("gameoflife", "i32", [g, np.zeros_like(g)], 8)
+    live = {tuple(x) for x in np.argwhere(res[idx] == 1)}
+    assert live == {(r + 2, c + 127) for r, c in [(1, 2), (2, 3), (3, 1), (3, 2), (3, 3)]}
+
+
+# ----------------------------------------------------- BASELINE configs
+def test_config0_jacobi_512_x10(oracle):
+    f = inputs.generate_np((512, 512), "f32", inputs.BASE_SEED + 0)
+    bufs = [f.copy(), np.zeros_like(f)]
+    ridx = oracle.run("jacobi2d5", "f32", bufs, 10)
+    gidx, gb = gpu_run("jacobi2d5", "f32", [f.copy(), np.zeros_like(f)], 10)
+    assert_parity(gb[gidx], bufs[ridx], "f32", "jacobi 512^2 x 10")
+
+
+WINDOWS_8192 = [(slice(0, 48), slice(0, 160)), (slice(4000, 4064), slice(4090, 4230)),
+                (slice(8150, 8192), slice(8000, 8192)), (slice(2, 40), slice(8060, 8192))]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("variant", ["shuffle", "plain"])
+def test_config1_gaussblur_8192_x100_windows(oracle, variant):
+    shape = (8192, 8192)
+    f = inputs.generate_np(shape, "f32", inputs.BASE_SEED + 1)
+    gidx, gb = gpu_run("gaussblur5x5", "f32", [f, np.zeros_like(f)], 100, variant=variant)
+    for w in WINDOWS_8192:
+        ref = oracle_window_run(oracle, "gaussblur5x5", "f32", [f, np.zeros_like(f)], 100, w, 2,
+                                nthreads=8)
+        assert_parity(gb[gidx][w], ref, "f32", f"gaussblur 8192^2 x100 window {w}")
+
+
+@pytest.mark.slow
+def test_config3_gameoflife_16384_x10_windows(oracle):
+    shape = (16384, 16384)
+    f = inputs.generate_np(shape, "i32", inputs.BASE_SEED + 3)
+    gidx, gb = gpu_run("gameoflife", "i32", [f, np.zeros_like(f)], 10)
+    rng = np.random.default_rng(0)
+    wins = [(slice(0, 64), slice(0, 256)), (slice(16320, 16384), slice(16128, 16384))]
+    for _ in range(6):
+        y, x = rng.integers(0, 16384 - 256, size=2)
+        wins.append((slice(int(y), int(y) + 64), slice(int(x), int(x) + 256)))
+    for w in wins:
+        ref = oracle_window_run(oracle, "gameoflife", "i32", [f, np.zeros_like(f)], 10, w, 1)
+        assert_parity(gb[gidx][w], ref, "i32", f"life window {w}")
