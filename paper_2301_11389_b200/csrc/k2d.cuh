@@ -11,42 +11,47 @@
 //  * S1 map: a warp owns one x-tile of 32 lanes x V elements (one 16-byte
 //    vector per lane: 128 fp32/int32 or 64 fp64 points) and marches down a
 //    strip of H rows (the slow axis y).  A CTA holds kWarps2D adjacent
-//    x-tiles of the same strip, so warp-edge fallback loads hit L1.
-//  * S2 row-tile load: one coalesced LDG.128 per lane per row, issued D rows
-//    ahead into a register ring of NS = 2R+1+D rows (software pipeline).
-//  * S3 x-neighbour taps: the R elements left / right of a lane's vector.
-//      SHUFFLE: shfl.sync.up/down by one lane (N = -1 / +1 in lane units).
-//      PLAIN:   loads of the same elements (L1-resident: the neighbour lane
-//               loaded that line in the same instruction).
-//  * S4 corner cases: lane 0 / lane 31 take their outer halo from a
-//    predicated load (the %out_of_range fallback); lanes past the row end
-//    clamp their address (the warp stays full, no %incomplete case) and
-//    their stores are masked.  No branch is divergent except the store mask
-//    in the two edge tiles of a row.
-//  * S5 slow-axis taps: the ring keeps the 2R+1 rows of the y-window in
-//    registers; a row is loaded from HBM exactly once per strip.
+//    x-tiles of the same strip.
+//  * S2 row-tile load: lane 0 of each warp streams the warp's row segment
+//    (its 32*V elements plus a 16-byte pad each side) into a per-warp ring of
+//    kStages2D shared-memory rows with cp.async.bulk (TMA bulk copy, SASS
+//    UBLKCP) completing on one mbarrier per stage; ~kStages2D rows per warp
+//    are in flight without holding registers.  Every input element is read
+//    from HBM once per strip.
+//  * S3 x-neighbour taps: each lane reads its own 16-byte vector (LDS.128)
+//    into the register window; the R elements left / right of it:
+//      SHUFFLE: shfl.sync.up/down by one lane (N = -1 / +1 in lane units);
+//      PLAIN:   loads of the same elements from the staged row (LDS).
+//  * S4 corner cases: in SHUFFLE lane 0 / lane 31 take their outer halo from
+//    the staged row (the %out_of_range fallback load);
+//    lanes past the row end read unused pad (the warp stays full: no
+//    %incomplete case) and their stores are masked.  The only divergent
+//    branch is the store mask in the two edge tiles of a row.
+//  * S5 slow-axis taps: the 2R+1 rows of the y-window live in registers,
+//    rotated by unrolling (no register moves).
 //  * S6 arithmetic: Op::point on the register window, identical code for
 //    both variants (so SHUFFLE == PLAIN bit for bit).
 //  * S7 store: STG.128 of interior points; the boundary ring is never
 //    written.
 #pragma once
 #include "common.cuh"
+#include "pipe.cuh"
 
 namespace stb200 {
 
 constexpr int kWarps2D = 4;       // x-tiles per CTA (128 threads)
-constexpr int kDepth2D = 3;       // rows in flight per warp (prefetch distance)
+constexpr int kStages2D = 8;      // staged rows per warp (bulk copies in flight)
 
 enum { VAR_SHUFFLE = 0, VAR_PLAIN = 1 };
 
 // Read-only view of the register window for output row y at unroll phase u:
 // w(dj, e) = element e (0 .. V+2R-1, centre of output p at e = p+R) of input
 // row y+dj.  All indices fold to constants after unrolling.
-template <typename T, int NS, int W, int R>
+template <typename T, int NW, int W, int R>
 struct Win {
-    const T (&a)[NS][W];
+    const T (&a)[NW][W];
     int u;
-    __device__ __forceinline__ T operator()(int dj, int e) const { return a[(u + R + dj) % NS][e]; }
+    __device__ __forceinline__ T operator()(int dj, int e) const { return a[(u + R + dj) % NW][e]; }
 };
 
 // ---------------------------------------------------------------- stencils
@@ -108,66 +113,121 @@ struct OpLife {
 };
 
 // ------------------------------------------------------------------ kernel
+// Shared memory per warp: kStages2D rows of WS = 32*V + 2*PAD elements, PAD =
+// one 16-byte vector, + kStages2D mbarriers.
+template <typename T>
+constexpr int k2d_row_elems() { return 32 * vlen<T>() + 2 * vlen<T>(); }
+template <typename T>
+constexpr size_t k2d_smem_bytes() {
+    return (size_t)kWarps2D * kStages2D * (k2d_row_elems<T>() * sizeof(T) + sizeof(uint64_t));
+}
+
 // Grid: x = ceil(ntiles / kWarps2D), y = strips of H output rows covering
 // output rows [y_lo, y_hi) (R <= y_lo, y_hi <= ny - R).
-template <class Op, typename T, int VARIANT, int D = kDepth2D>
+template <class Op, typename T, int VARIANT>
 __global__ void __launch_bounds__(kWarps2D * 32)
 k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_hi, int H,
     Coeffs<T, Op::NC> c) {
     constexpr int R = Op::R;
     constexpr int V = vlen<T>();
-    constexpr int W = V + 2 * R;          // lane window width: halo | vector | halo
-    constexpr int NS = 2 * R + 1 + D;     // register ring: y-window + rows in flight
-    static_assert(R <= V, "halo wider than one lane vector");
+    constexpr int PAD = V;                 // 16 bytes of halo room each side
+    constexpr int W = V + 2 * R;           // lane window width: halo | vector | halo
+    constexpr int NW = 2 * R + 1;          // register y-window
+    constexpr int WS = k2d_row_elems<T>();
+    constexpr int S = kStages2D;
+    static_assert(R <= PAD, "halo wider than the staging pad");
 
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5;
     const int lane = lane_id();
-    const int64_t x0 = ((int64_t)blockIdx.x * kWarps2D + (threadIdx.x >> 5)) * (32 * V);
+    T* ring = reinterpret_cast<T*>(smem_raw) + (size_t)warp * S * WS;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kWarps2D * S * WS * sizeof(T)) +
+                     warp * S;
+
+    const int64_t x0 = ((int64_t)blockIdx.x * kWarps2D + warp) * (32 * V);
     if (x0 >= nx) return;                                   // warp-uniform
     const int ys = y_lo + (int)blockIdx.y * H;
     const int ye = min(ys + H, y_hi);
     if (ys >= ye) return;
-    const int row_end = ye + R;                            // rows [ys-R, ye+R) are read
+    const int row0 = ys - R;                               // first input row of the strip
+    const int nrows = ye - ys + 2 * R;                     // input rows [ys-R, ye+R)
+
+    // Row segment [x0-PAD, x0+32V+PAD) clipped to [0, nx): 16-byte aligned.
+    const int64_t g_lo = x0 - PAD > 0 ? x0 - PAD : 0;
+    const int64_t g_hi = x0 + 32 * V + PAD < nx ? x0 + 32 * V + PAD : nx;
+    const uint32_t seg_bytes = (uint32_t)((g_hi - g_lo) * (int64_t)sizeof(T));
+    const int s_off = (int)(g_lo - (x0 - PAD));            // smem element of g_lo
+
+    if (lane == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        fence_barrier_init();
+    }
+    __syncwarp();
+    auto issue = [&](int r) {                              // lane 0 only
+        const int s = r % S;
+        mbar_arrive_expect_tx(&bars[s], seg_bytes);
+        bulk_g2s(ring + s * WS + s_off, in + (int64_t)(row0 + r) * nx + g_lo, seg_bytes, &bars[s]);
+    };
+    if (lane == 0) {
+        for (int r = 0; r < S && r < nrows; ++r) issue(r);
+    }
 
     const int64_t xl = x0 + lane * V;                      // first column of this lane
     const bool own = xl < nx;
-    const int64_t xr = own ? xl : nx - V;                  // clamped: the warp stays full
-    const bool left_edge = lane == 0 && x0 - R >= 0;       // %out_of_range, N = -1
-    const bool right_edge = lane == 31 && x0 + 32 * V < nx; // %out_of_range, N = +1
+    T win[NW][W];
 
-    T win[NS][W];
-
-    auto load = [&](int s, int row) {                       // S2
-        if (row < row_end) ldg_vec(&win[s][R], in + (int64_t)row * nx + xr);
-    };
-    auto finalize = [&](int s, int row) {                   // S3 + S4
-        const T* rp = in + (int64_t)row * nx;
+    // S2..S4: row r of the strip -> register window slot `slot`.
+    auto consume = [&](int r, T* dst) {
+        const int s = r % S;
+        mbar_wait(&bars[s], (uint32_t)(r / S) & 1u);
+        const T* row = ring + s * WS + PAD;                // element 0 = column x0
+        T v[V];
+        {
+            using VT = typename VecOf<T>::type;
+            const VT t = *reinterpret_cast<const VT*>(row + lane * V);
+            if constexpr (V == 4) { v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w; }
+            else { v[0] = t.x; v[1] = t.y; }
+        }
+#pragma unroll
+        for (int k = 0; k < V; ++k) dst[R + k] = v[k];
         if constexpr (VARIANT == VAR_SHUFFLE) {
 #pragma unroll
-            for (int k = 0; k < R; ++k) win[s][k] = shfl_up(win[s][V + k], 1);
+            for (int k = 0; k < R; ++k) dst[k] = shfl_up(v[V - R + k], 1);
 #pragma unroll
-            for (int k = 0; k < R; ++k) win[s][R + V + k] = shfl_down(win[s][R + k], 1);
-            if (left_edge) ldg_run<T, R>(&win[s][0], rp + x0 - R);
-            if (right_edge) ldg_run<T, R>(&win[s][R + V], rp + x0 + 32 * V);
+            for (int k = 0; k < R; ++k) dst[R + V + k] = shfl_down(v[k], 1);
+            if (lane == 0) {                                // warp edge: the fallback load
+#pragma unroll
+                for (int k = 0; k < R; ++k) dst[k] = row[k - R];
+            }
+            if (lane == 31) {
+#pragma unroll
+                for (int k = 0; k < R; ++k) dst[R + V + k] = row[32 * V + k];
+            }
         } else {
-            if (xr - R >= 0) ldg_run<T, R>(&win[s][0], rp + xr - R);
-            if (xr + V + R <= nx) ldg_run<T, R>(&win[s][R + V], rp + xr + V);
+#pragma unroll
+            for (int k = 0; k < R; ++k) dst[k] = row[lane * V - R + k];
+#pragma unroll
+            for (int k = 0; k < R; ++k) dst[R + V + k] = row[lane * V + V + k];
+        }
+        __syncwarp();                                      // every lane has read stage s
+        if (lane == 0 && r + S < nrows) {
+            fence_proxy_async_smem();
+            issue(r + S);
         }
     };
 
 #pragma unroll
-    for (int s = 0; s < NS; ++s) load(s, ys - R + s);
-#pragma unroll
-    for (int s = 0; s < 2 * R; ++s) finalize(s, ys - R + s);
+    for (int r = 0; r < 2 * R; ++r) consume(r, win[r]);
 
     const bool vec_store = own && xl >= R && xl + V <= nx - R;
-    for (int y0 = ys; y0 < ye; y0 += NS) {
+    for (int y0 = ys; y0 < ye; y0 += NW) {
 #pragma unroll
-        for (int u = 0; u < NS; ++u) {
+        for (int u = 0; u < NW; ++u) {
             const int y = y0 + u;
             if (y < ye) {                                   // warp-uniform
-                finalize((u + 2 * R) % NS, y + R);
+                consume(y - ys + 2 * R, win[(u + 2 * R) % NW]);
                 T o[V];
-                const Win<T, NS, W, R> w{win, u};
+                const Win<T, NW, W, R> w{win, u};
 #pragma unroll
                 for (int p = 0; p < V; ++p) o[p] = Op::point(w, p, c);   // S6
                 T* orow = out + (int64_t)y * nx;
@@ -178,7 +238,6 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
                     for (int p = 0; p < V; ++p)
                         if (xl + p >= R && xl + p < nx - R) orow[xl + p] = o[p];
                 }
-                load(u, y + R + D + 1);                     // the slot of row y-R
             }
         }
     }
