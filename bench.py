@@ -86,15 +86,20 @@ class ClockSampler:
         self.dev = device_index
         self.proc = None
         self.lines = []
+        self.n0 = 0
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()                 # nvidia-smi takes a moment to start
+            while not self.lines and time.time() - t0 < 5 and self.proc.poll() is None:
+                time.sleep(0.01)
+            self.n0 = len(self.lines)
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
@@ -105,6 +110,7 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            time.sleep(0.15)                 # one more sample covering the region's end
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -114,7 +120,7 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in self.lines[max(0, self.n0 - 1):]:
             p = [x.strip() for x in ln.split(",")]
             if len(p) < 7:
                 continue
@@ -214,7 +220,7 @@ def run_reference(args, wl, world, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="gaussblur", choices=sorted(WORKLOADS))
     ap.add_argument("--variant", default="shuffle", choices=["shuffle", "plain"])

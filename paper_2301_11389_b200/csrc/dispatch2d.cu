@@ -30,7 +30,7 @@ static cudaError_t launch_k2d(const stencil_s* h, const void* in, void* out, cud
     if (!blocks_per_sm) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern,
-                                                                      kWarps2D * 32, smem);
+                                                                      k2d_threads(), smem);
         if (e != cudaSuccess || blocks_per_sm < 1) blocks_per_sm = 1;
     }
     const int64_t nx = h->ldims[0], ny = h->ldims[1];
@@ -47,7 +47,7 @@ static cudaError_t launch_k2d(const stencil_s* h, const void* in, void* out, cud
     nstrips = (rows + H - 1) / H;
     Coeffs<T, Op::NC> c{};
     for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)h->coeffs[t];
-    kern<<<dim3((unsigned)gx, (unsigned)nstrips), kWarps2D * 32, smem, s>>>(
+    kern<<<dim3((unsigned)gx, (unsigned)nstrips), k2d_threads(), smem, s>>>(
         (const T*)in, (T*)out, nx, (int)y_lo, (int)y_hi, (int)H, c);
     return cudaGetLastError();
 }

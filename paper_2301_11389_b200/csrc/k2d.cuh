@@ -12,12 +12,11 @@
 //    vector per lane: 128 fp32/int32 or 64 fp64 points) and marches down a
 //    strip of H rows (the slow axis y).  A CTA holds kWarps2D adjacent
 //    x-tiles of the same strip.
-//  * S2 row-tile load: lane 0 of each warp streams the warp's row segment
-//    (its 32*V elements plus a 16-byte pad each side) into a per-warp ring of
-//    kStages2D shared-memory rows with cp.async.bulk (TMA bulk copy, SASS
-//    UBLKCP) completing on one mbarrier per stage; ~kStages2D rows per warp
-//    are in flight without holding registers.  Every input element is read
-//    from HBM once per strip.
+//  * S2 row-tile load: a producer warp streams the CTA's row segment into a
+//    ring of kStages2D shared-memory rows with cp.async.bulk (TMA bulk copy,
+//    SASS UBLKCP) completing on mbarriers; kStages2D rows per CTA are in
+//    flight without holding registers.  Every input element is read from HBM
+//    once per strip.
 //  * S3 x-neighbour taps: each lane reads its own 16-byte vector (LDS.128)
 //    into the register window; the R elements left / right of it:
 //      SHUFFLE: shfl.sync.up/down by one lane (N = -1 / +1 in lane units);
@@ -40,7 +39,7 @@
 namespace stb200 {
 
 constexpr int kWarps2D = 4;       // x-tiles per CTA (128 threads)
-constexpr int kStages2D = 8;      // staged rows per warp (bulk copies in flight)
+constexpr int kStages2D = 8;      // staged rows per CTA (bulk copies in flight); power of 2
 
 enum { VAR_SHUFFLE = 0, VAR_PLAIN = 1 };
 
@@ -113,19 +112,24 @@ struct OpLife {
 };
 
 // ------------------------------------------------------------------ kernel
-// Shared memory per warp: kStages2D rows of WS = 32*V + 2*PAD elements, PAD =
-// one 16-byte vector, + kStages2D mbarriers.
+// CTA = kWarps2D consumer warps (adjacent x-tiles of one strip) + 1 producer
+// warp.  The producer's elected lane streams the CTA's row segment (its
+// kWarps2D*32*V elements plus a 16-byte pad each side, 2 KiB + 32 B for
+// fp32) into a ring of kStages2D shared-memory rows with cp.async.bulk,
+// completion on a "full" mbarrier per stage; consumers release a stage on its
+// "empty" mbarrier (every consumer lane arrives: no divergent branch).
 template <typename T>
-constexpr int k2d_row_elems() { return 32 * vlen<T>() + 2 * vlen<T>(); }
+constexpr int k2d_row_elems() { return kWarps2D * 32 * vlen<T>() + 2 * vlen<T>(); }
 template <typename T>
 constexpr size_t k2d_smem_bytes() {
-    return (size_t)kWarps2D * kStages2D * (k2d_row_elems<T>() * sizeof(T) + sizeof(uint64_t));
+    return (size_t)kStages2D * (k2d_row_elems<T>() * sizeof(T) + 2 * sizeof(uint64_t));
 }
+constexpr int k2d_threads() { return (kWarps2D + 1) * 32; }
 
 // Grid: x = ceil(ntiles / kWarps2D), y = strips of H output rows covering
 // output rows [y_lo, y_hi) (R <= y_lo, y_hi <= ny - R).
 template <class Op, typename T, int VARIANT>
-__global__ void __launch_bounds__(kWarps2D * 32)
+__global__ void __launch_bounds__(k2d_threads())
 k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_hi, int H,
     Coeffs<T, Op::NC> c) {
     constexpr int R = Op::R;
@@ -136,55 +140,71 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
     constexpr int WS = k2d_row_elems<T>();
     constexpr int S = kStages2D;
     static_assert(R <= PAD, "halo wider than the staging pad");
+    static_assert((S & (S - 1)) == 0, "stage count must be a power of two");
+    constexpr unsigned LOG2S = S == 2 ? 1 : S == 4 ? 2 : S == 8 ? 3 : S == 16 ? 4 : 5;
 
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* ring = reinterpret_cast<T*>(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * WS * sizeof(T));
+    uint64_t* empty = full + S;
+
     const int warp = threadIdx.x >> 5;
     const int lane = lane_id();
-    T* ring = reinterpret_cast<T*>(smem_raw) + (size_t)warp * S * WS;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kWarps2D * S * WS * sizeof(T)) +
-                     warp * S;
-
-    const int64_t x0 = ((int64_t)blockIdx.x * kWarps2D + warp) * (32 * V);
-    if (x0 >= nx) return;                                   // warp-uniform
+    const int64_t X0 = (int64_t)blockIdx.x * (kWarps2D * 32 * V);   // CTA's first column
     const int ys = y_lo + (int)blockIdx.y * H;
     const int ye = min(ys + H, y_hi);
-    if (ys >= ye) return;
+    if (ys >= ye) return;                                  // CTA-uniform
     const int row0 = ys - R;                               // first input row of the strip
     const int nrows = ye - ys + 2 * R;                     // input rows [ys-R, ye+R)
+    const int64_t nt_left = (nx - X0 + 32 * V - 1) / (32 * V);
+    const int active = nt_left < kWarps2D ? (int)nt_left : kWarps2D;
 
-    // Row segment [x0-PAD, x0+32V+PAD) clipped to [0, nx): 16-byte aligned.
-    const int64_t g_lo = x0 - PAD > 0 ? x0 - PAD : 0;
-    const int64_t g_hi = x0 + 32 * V + PAD < nx ? x0 + 32 * V + PAD : nx;
-    const uint32_t seg_bytes = (uint32_t)((g_hi - g_lo) * (int64_t)sizeof(T));
-    const int s_off = (int)(g_lo - (x0 - PAD));            // smem element of g_lo
-
-    if (lane == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], active * 32);
+        }
         fence_barrier_init();
     }
-    __syncwarp();
-    auto issue = [&](int r) {                              // lane 0 only
-        const int s = r % S;
-        mbar_arrive_expect_tx(&bars[s], seg_bytes);
-        bulk_g2s(ring + s * WS + s_off, in + (int64_t)(row0 + r) * nx + g_lo, seg_bytes, &bars[s]);
-    };
-    if (lane == 0) {
-        for (int r = 0; r < S && r < nrows; ++r) issue(r);
-    }
+    __syncthreads();
 
+    if (warp == kWarps2D) {                                // ---- producer warp
+        if (lane == 0) {
+            // Row segment [X0-PAD, X0+kWarps2D*32V+PAD) clipped to [0, nx).
+            const int64_t g_lo = X0 - PAD > 0 ? X0 - PAD : 0;
+            const int64_t g_hi0 = X0 + kWarps2D * 32 * V + PAD;
+            const int64_t g_hi = g_hi0 < nx ? g_hi0 : nx;
+            const uint32_t bytes = (uint32_t)((g_hi - g_lo) * (int64_t)sizeof(T));
+            T* dst0 = ring + (g_lo - (X0 - PAD));
+            const T* src = in + (int64_t)row0 * nx + g_lo;
+            for (unsigned r = 0; r < (unsigned)nrows; ++r, src += nx) {
+                const unsigned s = r & (S - 1);
+                if (r >= S) mbar_wait(&empty[s], ((r >> LOG2S) - 1) & 1u);
+                mbar_arrive_expect_tx(&full[s], bytes);
+                bulk_g2s(dst0 + s * WS, src, bytes, &full[s]);
+            }
+        }
+        return;
+    }
+    if (warp >= active) return;                            // past the row end
+
+    // ---- consumer warps
+    const int64_t x0 = X0 + warp * (32 * V);
     const int64_t xl = x0 + lane * V;                      // first column of this lane
     const bool own = xl < nx;
+    const int lo_e = PAD + warp * 32 * V + lane * V;       // smem element of column xl
     T win[NW][W];
 
-    // S2..S4: row r of the strip -> register window slot `slot`.
-    auto consume = [&](int r, T* dst) {
-        const int s = r % S;
-        mbar_wait(&bars[s], (uint32_t)(r / S) & 1u);
-        const T* row = ring + s * WS + PAD;                // element 0 = column x0
+    const bool lane0 = lane == 0, lane31 = lane == 31;
+    // S2..S4: strip row r -> register window row dst
+    auto consume = [&](unsigned r, T* dst) {
+        const unsigned s = r & (S - 1);
+        mbar_wait(&full[s], (r >> LOG2S) & 1u);
+        const T* row = ring + s * WS;
         T v[V];
         {
             using VT = typename VecOf<T>::type;
-            const VT t = *reinterpret_cast<const VT*>(row + lane * V);
+            const VT t = *reinterpret_cast<const VT*>(row + lo_e);
             if constexpr (V == 4) { v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w; }
             else { v[0] = t.x; v[1] = t.y; }
         }
@@ -195,52 +215,76 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
             for (int k = 0; k < R; ++k) dst[k] = shfl_up(v[V - R + k], 1);
 #pragma unroll
             for (int k = 0; k < R; ++k) dst[R + V + k] = shfl_down(v[k], 1);
-            if (lane == 0) {                                // warp edge: the fallback load
+            // warp-edge lanes: the fallback load, from the
+            // staged row; a select of two loaded values keeps it branch-free
+            const int e = lane0 ? lo_e - R : lo_e + V;
+            T hv[R];
 #pragma unroll
-                for (int k = 0; k < R; ++k) dst[k] = row[k - R];
-            }
-            if (lane == 31) {
+            for (int k = 0; k < R; ++k) hv[k] = row[e + k];
 #pragma unroll
-                for (int k = 0; k < R; ++k) dst[R + V + k] = row[32 * V + k];
+            for (int k = 0; k < R; ++k) {
+                dst[k] = lane0 ? hv[k] : dst[k];
+                dst[R + V + k] = lane31 ? hv[k] : dst[R + V + k];
             }
         } else {
 #pragma unroll
-            for (int k = 0; k < R; ++k) dst[k] = row[lane * V - R + k];
+            for (int k = 0; k < R; ++k) dst[k] = row[lo_e - R + k];
 #pragma unroll
-            for (int k = 0; k < R; ++k) dst[R + V + k] = row[lane * V + V + k];
+            for (int k = 0; k < R; ++k) dst[R + V + k] = row[lo_e + V + k];
         }
-        __syncwarp();                                      // every lane has read stage s
-        if (lane == 0 && r + S < nrows) {
-            fence_proxy_async_smem();
-            issue(r + S);
-        }
+        mbar_arrive(&empty[s]);                           // this lane is done with stage s
     };
 
-#pragma unroll
-    for (int r = 0; r < 2 * R; ++r) consume(r, win[r]);
-
+    // S7 masks: whole-vector store for lanes fully inside the interior, else
+    // per-element stores of the interior columns (edge tiles only).  Warps
+    // whose lanes are all interior take a loop without the element stores.
     const bool vec_store = own && xl >= R && xl + V <= nx - R;
-    for (int y0 = ys; y0 < ye; y0 += NW) {
+    bool el_store[V];
 #pragma unroll
-        for (int u = 0; u < NW; ++u) {
-            const int y = y0 + u;
-            if (y < ye) {                                   // warp-uniform
-                consume(y - ys + 2 * R, win[(u + 2 * R) % NW]);
-                T o[V];
-                const Win<T, NW, W, R> w{win, u};
+    for (int p = 0; p < V; ++p) el_store[p] = !vec_store && own && xl + p >= R && xl + p < nx - R;
+    Coeffs<T, Op::NC> cr;                                  // coefficients held in registers
 #pragma unroll
-                for (int p = 0; p < V; ++p) o[p] = Op::point(w, p, c);   // S6
-                T* orow = out + (int64_t)y * nx;
-                if (vec_store) {
-                    stg_vec(orow + xl, o);                              // S7
-                } else if (own) {
+    for (int t = 0; t < Op::NC; ++t) cr.c[t] = c.c[t];
+
 #pragma unroll
-                    for (int p = 0; p < V; ++p)
-                        if (xl + p >= R && xl + p < nx - R) orow[xl + p] = o[p];
-                }
+    for (int r = 0; r < 2 * R; ++r) consume((unsigned)r, win[r]);
+
+    auto sweep = [&](auto edge_tag) {
+        constexpr bool EDGE = decltype(edge_tag)::value;
+        T* optr = out + (int64_t)ys * nx + xl;             // running output pointer
+        auto emit = [&](int u) {
+            T o[V];
+            const Win<T, NW, W, R> w{win, u};
+#pragma unroll
+            for (int p = 0; p < V; ++p) o[p] = Op::point(w, p, cr);      // S6
+            if constexpr (!EDGE) {
+                stg_vec(optr, o);                                       // S7
+            } else {
+                if (vec_store) stg_vec(optr, o);
+#pragma unroll
+                for (int p = 0; p < V; ++p)
+                    if (el_store[p]) optr[p] = o[p];
+            }
+            optr += nx;
+        };
+        int y = ys;
+        for (; y + NW <= ye; y += NW) {                    // full groups: no guards
+#pragma unroll
+            for (int u = 0; u < NW; ++u) {
+                consume((unsigned)(y + u - ys + 2 * R), win[(u + 2 * R) % NW]);
+                emit(u);
             }
         }
-    }
+#pragma unroll
+        for (int u = 0; u < NW - 1; ++u) {                 // remainder (< NW rows)
+            if (y + u < ye) {
+                consume((unsigned)(y + u - ys + 2 * R), win[(u + 2 * R) % NW]);
+                emit(u);
+            }
+        }
+    };
+    if (__all_sync(FULL, vec_store)) sweep(std::false_type{});
+    else sweep(std::true_type{});
 }
 
 }  // namespace stb200
