@@ -1,11 +1,131 @@
-// dispatch3d.cu — host launchers of the 3-D kernels (k3d.cuh).
+// dispatch3d.cu — host launchers of the 3-D kernels (k3d.cuh): TMA tensor
+// maps (cuTensorMapEncodeTiled through the runtime's driver entry point, no
+// libcuda link), one-wave grid sizing, variant selection.
+#include <cudaTypedefs.h>
+
 #include "internal.h"
+#include "k3d.cuh"
+#include "ktricubic.cuh"
 
 namespace stb200 {
 
-cudaError_t dispatch_3d(stencil_s*, const void* const*, void* const*, cudaStream_t, int64_t,
-                        int64_t) {
-    return cudaErrorNotSupported;
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
 }
 
+// 3-D tensor map over a dense (nz, ny, nx) array, box (bx, by, 1), zero OOB fill.
+static cudaError_t make_tmap(CUtensorMap* m, const void* base, int dtype, const int64_t* ld, int bx, int by) {
+    auto fn = encode_fn();
+    if (!fn) return cudaErrorNotSupported;
+    const size_t es = dtype == ST_F64 ? 8 : 4;
+    cuuint64_t gdim[3] = {(cuuint64_t)ld[0], (cuuint64_t)ld[1], (cuuint64_t)ld[2]};
+    cuuint64_t gstride[2] = {(cuuint64_t)ld[0] * es, (cuuint64_t)(ld[0] * ld[1]) * es};
+    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(m, dtype == ST_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                    const_cast<void*>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+int sm_count_of(int device) {
+    static int cached[64] = {0};
+    if (device < 0 || device >= 64) return 148;
+    if (!cached[device]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+        cached[device] = n > 0 ? n : 148;
+    }
+    return cached[device];
+}
+
+template <class Op, typename T, int VAR>
+static cudaError_t launch_k3d(const stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
+                              int64_t z_lo, int64_t z_hi) {
+    using L = Layout3<Op, T>;
+    auto kern = k3d<Op, T, VAR>;
+    constexpr size_t smem = L::smem_bytes();
+    static int blocks_per_sm = 0;
+    if (!blocks_per_sm) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, k3d_threads(), smem) !=
+                cudaSuccess || blocks_per_sm < 1)
+            blocks_per_sm = 1;
+    }
+    const int64_t* ld = h->ldims;
+    if (z_lo < 0) { z_lo = Op::R; z_hi = ld[2] - Op::R; }
+    if (z_hi <= z_lo) return cudaSuccess;
+    TmapPack<Op::NA> tm;
+    for (int a = 0; a < Op::NA; ++a) {
+        cudaError_t e = make_tmap(&tm.m[a], in[a], h->dtype, ld, L::bx(a), L::by(a));
+        if (e != cudaSuccess) return e;
+    }
+    K3Args<Op, T> args;
+    for (int k = 0; k < Op::NOUT; ++k) args.out[k] = (T*)out[k];
+    args.nx = ld[0];
+    args.ny = ld[1];
+    args.z_lo = (int)z_lo;
+    args.nzo = (int)(z_hi - z_lo);
+    args.ntx = (int)((ld[0] + L::TX - 1) / L::TX);
+    args.nty = (int)((ld[1] + L::TY - 1) / L::TY);
+    args.work = (int64_t)args.ntx * args.nty * args.nzo;
+    int64_t grid = (int64_t)blocks_per_sm * sm_count_of(h->device);
+    if (grid > args.work) grid = args.work;
+    Coeffs<T, Op::NC> c{};
+    for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)h->coeffs[t];
+    kern<<<(unsigned)grid, k3d_threads(), smem, s>>>(tm, args, c);
+    return cudaGetLastError();
+}
+
+template <template <typename> class OpT, typename T>
+static cudaError_t launch3_var(const stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
+                               int64_t a, int64_t b) {
+    if (h->variant == ST_PLAIN) return launch_k3d<OpT<T>, T, 1>(h, in, out, s, a, b);
+    return launch_k3d<OpT<T>, T, 0>(h, in, out, s, a, b);
+}
+
+cudaError_t launch_tricubic(const stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
+                            int64_t z_lo, int64_t z_hi);
+
+cudaError_t dispatch_3d(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
+                        int64_t a, int64_t b) {
+    const bool f64 = h->dtype == ST_F64;
+    switch (h->k->kind) {
+    case ST_LAPLACIAN3D7:
+    case ST_JACOBI3D7:
+        return f64 ? launch3_var<OpLap7, double>(h, in, out, s, a, b)
+                   : launch3_var<OpLap7, float>(h, in, out, s, a, b);
+    case ST_WAVE13PT:
+        return f64 ? launch3_var<OpWave13, double>(h, in, out, s, a, b)
+                   : launch3_var<OpWave13, float>(h, in, out, s, a, b);
+    case ST_GRADIENT:
+        return f64 ? launch3_var<OpGradient, double>(h, in, out, s, a, b)
+                   : launch3_var<OpGradient, float>(h, in, out, s, a, b);
+    case ST_DIVERGENCE:
+        return f64 ? launch3_var<OpDivergence, double>(h, in, out, s, a, b)
+                   : launch3_var<OpDivergence, float>(h, in, out, s, a, b);
+    case ST_TRICUBIC:
+        return launch_tricubic(h, in, out, s, a, b);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace stb200
+
+namespace stb200 {
+cudaError_t launch_tricubic(const stencil_s*, const void* const*, void* const*, cudaStream_t, int64_t,
+                            int64_t) {
+    return cudaErrorNotSupported;
+}
 }  // namespace stb200

@@ -97,7 +97,23 @@ template <typename T> struct OpGauss5 {
         for (int t = 1; t < 25; ++t) acc = fma(c.c[t], w(t / 5 - 2, p + t % 5), acc);
         return acc;
     }
+    // fp32: two adjacent outputs (p, p+1) per packed FFMA2 (fma.rn.f32x2):
+    // the same per-point FMA chain as point(), half the issue slots.
+    static constexpr bool kPaired = std::is_same<T, float>::value;
+    template <class Wn>
+    __device__ __forceinline__ static float2 point2(const Wn& w, int p, const Coeffs<T, NC>& c) {
+        float2 acc = __fmul2_rn(make_float2(c.c[0], c.c[0]), make_float2(w(-2, p), w(-2, p + 1)));
+#pragma unroll
+        for (int t = 1; t < 25; ++t) {
+            const int dj = t / 5 - 2, e = p + t % 5;
+            acc = __ffma2_rn(make_float2(c.c[t], c.c[t]), make_float2(w(dj, e), w(dj, e + 1)), acc);
+        }
+        return acc;
+    }
 };
+
+template <class Op, class = void> struct HasPaired : std::false_type {};
+template <class Op> struct HasPaired<Op, std::enable_if_t<Op::kPaired>> : std::true_type {};
 
 // gameoflife: Conway B3/S23 on int cells (Table 1, 9 loads)
 struct OpLife {
@@ -256,7 +272,17 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
             T o[V];
             const Win<T, NW, W, R> w{win, u};
 #pragma unroll
-            for (int p = 0; p < V; ++p) o[p] = Op::point(w, p, cr);      // S6
+            if constexpr (HasPaired<Op>::value) {                       // S6
+#pragma unroll
+                for (int p = 0; p < V; p += 2) {
+                    const float2 r = Op::point2(w, p, cr);
+                    o[p] = r.x;
+                    o[p + 1] = r.y;
+                }
+            } else {
+#pragma unroll
+                for (int p = 0; p < V; ++p) o[p] = Op::point(w, p, cr);
+            }
             if constexpr (!EDGE) {
                 stg_vec(optr, o);                                       // S7
             } else {

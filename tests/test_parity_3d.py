@@ -1,0 +1,181 @@
+"""GPU parity of the 3-D kernels (TMA plane ring) against the CPU oracle.
+
+Small grids spanning several x-tiles (128 fp32 / 64 fp64), several CTA row
+tiles (8 rows), ragged tails in every axis and the minimum grids; SHUFFLE vs
+PLAIN bit identity; runs (ping-pong, the wave13pt 3-level rotation, repeated
+steps); closed-form pins on the device; and the BASELINE configs at full
+size on dependence-cone windows (laplacian / wave13pt fp64 512^3, jacobi3d
+fp32 1024^3, divergence / gradient fp32 512^3), in bench.py's launch
+configuration.
+"""
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2301_11389_b200 import inputs
+from parity import (assert_parity, gpu_run, gpu_step, interior, oracle_window_run, ring_mask)
+
+pytestmark = pytest.mark.gpu
+
+KINDS_3D = ["laplacian3d7", "jacobi3d7", "wave13pt", "divergence", "gradient"]
+SHAPES = {  # (nz, ny, nx) numpy order
+    "f32": [(3, 3, 4), (5, 5, 8), (7, 9, 36), (12, 17, 132), (10, 33, 260), (6, 8, 516)],
+    "f64": [(3, 3, 4), (5, 5, 6), (6, 11, 66), (9, 13, 130), (7, 20, 258)],
+}
+
+
+def cases():
+    for kind in KINDS_3D:
+        r = 2 if kind == "wave13pt" else 1
+        for dt in ("f32", "f64"):
+            for shape in SHAPES[dt]:
+                if min(shape) >= 2 * r + 1:
+                    yield kind, dt, shape
+
+
+def seed_of(*key):
+    return inputs.BASE_SEED + zlib.crc32(repr(key).encode()) % 1000
+
+
+@pytest.mark.parametrize("kind,dtype,shape", list(cases()),
+                         ids=lambda v: v if isinstance(v, str) else "x".join(map(str, v)))
+def test_step_parity_and_variants(oracle, kind, dtype, shape):
+    ar = oracle.arity(kind)
+    ins = [inputs.generate_np(shape, dtype, seed_of(kind, dtype, shape), a)
+           for a in range(ar["n_in"])]
+    refs = [np.zeros_like(ins[0]) for _ in range(ar["n_out"])]
+    oracle.step(kind, dtype, ins, refs)
+    sl = interior(shape, ar["lo"], ar["hi"])
+    outs = {}
+    for var in ("shuffle", "plain"):
+        gs = gpu_step(kind, dtype, ins, ar["n_out"], variant=var, fill=0)
+        for k, (g, r) in enumerate(zip(gs, refs)):
+            assert_parity(g[sl], r[sl], dtype, f"{kind} {dtype} {shape} {var} out{k}")
+            assert np.all(g[ring_mask(shape, ar["lo"], ar["hi"])] == 0), "boundary written"
+        outs[var] = gs
+    for a, b in zip(outs["shuffle"], outs["plain"]):
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), "SHUFFLE and PLAIN differ"
+
+
+@pytest.mark.parametrize("kind,dtype,shape", [
+    ("laplacian3d7", "f64", (9, 13, 130)), ("jacobi3d7", "f32", (12, 17, 132)),
+    ("wave13pt", "f64", (10, 12, 66)), ("wave13pt", "f32", (9, 10, 132)),
+    ("divergence", "f32", (7, 9, 36)), ("gradient", "f64", (6, 11, 66))])
+def test_run_parity(oracle, kind, dtype, shape):
+    ar = oracle.arity(kind)
+    ins = [inputs.generate_np(shape, dtype, inputs.BASE_SEED + 5, a) for a in range(ar["n_in"])]
+    if ar["n_bufs"] == 2:
+        bufs = [ins[0], np.zeros_like(ins[0])]
+    elif kind == "wave13pt":
+        bufs = [ins[0], ins[1], np.zeros_like(ins[0])]
+    else:
+        bufs = ins + [np.zeros_like(ins[0]) for _ in range(ar["n_out"])]
+    ob = [b.copy() for b in bufs]
+    ridx = oracle.run(kind, dtype, ob, 5)
+    for var in ("shuffle", "plain"):
+        gidx, gb = gpu_run(kind, dtype, [b.copy() for b in bufs], 5, variant=var)
+        assert gidx == ridx
+        for k in range(ar["n_out"] if ar["n_bufs"] > 3 else 1):
+            assert_parity(gb[gidx + k], ob[ridx + k], dtype, f"{kind} run {var} out{k}")
+
+
+def test_laplacian_closed_form_on_gpu():
+    """i^2+j^2+k^2 -> 6 exactly; a linear field -> 0 exactly."""
+    k, j, i = np.meshgrid(np.arange(20.0), np.arange(24.0), np.arange(132.0), indexing="ij")
+    for f, v in (((i * i + j * j + k * k).astype(np.float32), 6.0),
+                 ((3 * i - 2 * j + k).astype(np.float32), 0.0)):
+        (g,) = gpu_step("laplacian3d7", "f32", [f], 1)
+        assert np.all(g[1:-1, 1:-1, 1:-1] == v)
+
+
+def test_divergence_gradient_closed_forms_on_gpu():
+    k, j, i = np.meshgrid(np.arange(10.0), np.arange(12.0), np.arange(68.0), indexing="ij")
+    (d,) = gpu_step("divergence", "f64", [i.copy(), j.copy(), k.copy()], 1)
+    assert np.all(d[1:-1, 1:-1, 1:-1] == 3.0)
+    gs = gpu_step("gradient", "f64", [3 * i - 2 * j + 5 * k], 3)
+    for g, v in zip(gs, (3.0, -2.0, 5.0)):
+        assert np.all(g[1:-1, 1:-1, 1:-1] == v)
+
+
+# ----------------------------------------------------- BASELINE configs
+def _dev_fields(shape, dtype, seed, n):
+    return [inputs.generate_torch(shape, dtype, seed, a) for a in range(n)]
+
+
+def _window_check(oracle, kind, dtype, dev_init, dev_result, n_iters, r, windows):
+    """Compare device results against the oracle on dependence-cone windows;
+    the oracle reads the initial fields' sub-blocks copied from the device."""
+    shape = tuple(dev_init[0].shape)
+    grow = (n_iters + 1) * r
+    for w in windows:
+        sub = tuple(slice(max(0, s.start - grow), min(n, s.stop + grow)) for s, n in zip(w, shape))
+        fields = [t[sub].cpu().numpy() for t in dev_init]
+        inner = tuple(slice(s.start - u.start, s.stop - u.start) for s, u in zip(w, sub))
+        full_w = tuple(slice(0, u.stop - u.start) for u in sub)
+        ref = oracle_window_run(oracle, kind, dtype, fields, n_iters, full_w, r, nthreads=8)
+        assert_parity(dev_result[w].cpu().numpy(), ref[inner], dtype, f"{kind} window {w}")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("kind,dtype,dims,iters", [
+    ("laplacian3d7", "f64", (512, 512, 512), 10), ("wave13pt", "f64", (512, 512, 512), 10),
+    ("jacobi3d7", "f32", (1024, 1024, 1024), 10)])
+def test_configs_full_size_windows(oracle, kind, dtype, dims, iters):
+    from paper_2301_11389_b200.binding import Stencil
+    shape = dims[::-1]
+    ar = oracle.arity(kind)
+    init = _dev_fields(shape, dtype, inputs.BASE_SEED + 2, ar["n_in"])
+    if kind == "wave13pt":
+        bufs = [init[0].clone(), init[1].clone(), torch.zeros_like(init[0])]
+        oinit = [init[0], init[1], torch.zeros_like(init[0])]
+    else:
+        bufs = [init[0].clone(), torch.zeros_like(init[0])]
+        oinit = [init[0], torch.zeros_like(init[0])]
+    st = Stencil(kind, dims, dtype)
+    idx = st.run(bufs, iters)
+    torch.cuda.synchronize()
+    r = ar["hi"]
+    n = shape[0]
+    wins = [(slice(0, 8), slice(0, 8), slice(0, 40)),
+            (slice(n // 2, n // 2 + 8), slice(n // 3, n // 3 + 8), slice(n - 70, n - 6)),
+            (slice(n - 8, n), slice(n - 8, n), slice(n - 40, n))]
+    _window_check(oracle, kind, dtype, oinit, bufs[idx], iters, r, wins)
+    st.close()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("kind", ["divergence", "gradient"])
+def test_suite_512_single_step_samples(oracle, kind):
+    from paper_2301_11389_b200.binding import Stencil
+    shape = (512, 512, 512)
+    ar = oracle.arity(kind)
+    ins = _dev_fields(shape, "f32", inputs.BASE_SEED + 9, ar["n_in"])
+    outs = [torch.zeros_like(ins[0]) for _ in range(ar["n_out"])]
+    st = Stencil(kind, shape[::-1], "f32")
+    st.step(ins, outs)
+    torch.cuda.synchronize()
+    for w in [(slice(0, 6), slice(0, 6), slice(0, 140)), (slice(250, 256), slice(500, 512),
+                                                           slice(380, 512))]:
+        sub = tuple(slice(max(0, s.start - 1), min(512, s.stop + 1)) for s in w)
+        f = [t[sub].cpu().numpy() for t in ins]
+        refs = [np.zeros_like(f[0]) for _ in range(ar["n_out"])]
+        oracle.step(kind, "f32", f, refs)
+        inner = tuple(slice(s.start - u.start, s.stop - u.start) for s, u in zip(w, sub))
+        # compare interior points of the window only
+        for k in range(ar["n_out"]):
+            g = outs[k][w].cpu().numpy()
+            rr = refs[k][inner]
+            m = np.zeros(g.shape, bool)
+            gi = [np.arange(s.start, s.stop) for s in w]
+            ok = [(a >= 1) & (a < 511) for a in gi]
+            m[np.ix_(*ok)] = True
+            sub_in = tuple(slice(s.start - u.start, s.stop - u.start) for s, u in zip(w, sub))
+            m &= np.ones_like(m)
+            # oracle only wrote its own interior: exclude the cut-out's ring
+            ring = np.zeros(f[0].shape, bool)
+            ring[1:-1, 1:-1, 1:-1] = True
+            m &= ring[sub_in]
+            assert_parity(g[m], rr[m], "f32", f"{kind} out{k} window {w}")
+    st.close()
