@@ -3,6 +3,8 @@
 // libcuda link), one-wave grid sizing, variant selection.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 #include "internal.h"
 #include "k3d.cuh"
 #include "ktricubic.cuh"
@@ -34,7 +36,7 @@ static cudaError_t make_tmap(CUtensorMap* m, const void* base, int dtype, const 
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = fn(m, dtype == ST_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                     const_cast<void*>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
@@ -72,6 +74,7 @@ static cudaError_t launch_k3d(const stencil_s* h, const void* const* in, void* c
         if (e != cudaSuccess) return e;
     }
     K3Args<Op, T> args;
+    for (int a = 0; a < Op::NA; ++a) args.in[a] = (const T*)in[a];
     for (int k = 0; k < Op::NOUT; ++k) args.out[k] = (T*)out[k];
     args.nx = ld[0];
     args.ny = ld[1];
@@ -79,9 +82,21 @@ static cudaError_t launch_k3d(const stencil_s* h, const void* const* in, void* c
     args.nzo = (int)(z_hi - z_lo);
     args.ntx = (int)((ld[0] + L::TX - 1) / L::TX);
     args.nty = (int)((ld[1] + L::TY - 1) / L::TY);
-    args.work = (int64_t)args.ntx * args.nty * args.nzo;
-    int64_t grid = (int64_t)blocks_per_sm * sm_count_of(h->device);
-    if (grid > args.work) grid = args.work;
+    // lockstep round robin (k3d.cuh LockIter): split z only when there are
+    // fewer columns than SMs; equal items per CTA; chunks of zc planes
+    const int64_t ncols = (int64_t)args.ntx * args.nty;
+    const int64_t slots = (int64_t)blocks_per_sm * sm_count_of(h->device);
+    int64_t zsplit = slots / ncols;
+    if (zsplit < 1) zsplit = 1;
+    if (zsplit > args.nzo) zsplit = args.nzo;
+    const int64_t items = ncols * zsplit;
+    const int64_t m = (items + slots - 1) / slots;
+    const int64_t grid = (items + m - 1) / m;
+    args.zsplit = (int)zsplit;
+    args.m = (int)m;
+    args.zc = 64;
+    static const int dbg = getenv("STB200_DBG") ? atoi(getenv("STB200_DBG")) : 0;
+    args.dbg = dbg;
     Coeffs<T, Op::NC> c{};
     for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)h->coeffs[t];
     kern<<<(unsigned)grid, k3d_threads(), smem, s>>>(tm, args, c);

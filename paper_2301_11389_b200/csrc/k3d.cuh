@@ -5,23 +5,26 @@
 // "We do not consider adjacent threads in non-leading dimensions"); the slow
 // axes are staged by the Tensor Memory Accelerator:
 //
-//  * S1 map: a CTA owns a column of the grid: an x-tile of 32*V elements (one
-//    16-byte vector per lane) by kWarps3D rows (one consumer warp per row),
-//    and marches along z.  The (column, z) work space is linearised and cut
-//    into one equal contiguous share per CTA (one wave, grid = resident CTAs
-//    = a multiple of the SM count), so every CTA streams the same number of
-//    planes; a share that crosses a column restarts the pipeline there.
+//  * S1 map: a CTA works on columns of the grid: an x-tile of 32*V elements
+//    (one 16-byte vector per lane) by kWarps3D*RY rows (RY consecutive rows
+//    per consumer warp), marching along z.  Grid = at most one CTA per SM (a
+//    persistent wave) with an equal number of (z part, column) items per CTA,
+//    walked in lockstep chunk by chunk (LockIter) so neighbouring tiles
+//    stream the same planes at the same time and share halo lines via L2; a
+//    chunk boundary restarts the pipeline (2R planes).
 //  * S2 plane load: a producer warp issues one TMA tensor copy
 //    (cp.async.bulk.tensor.3d, SASS UTMALDG) per staged array per z-plane: the
-//    box covers the tile plus a 16-byte x pad and R halo rows in y as the
-//    array needs; out-of-bounds parts are zero-filled by TMA and only ever
-//    feed masked (non-interior) outputs.  NS stages in a ring, full/empty
-//    mbarriers per stage.
+//    box is the tile's 512-byte rows plus one 32-byte sector each side (for
+//    arrays with x taps) and R halo rows in y (for arrays with y taps);
+//    out-of-bounds parts are zero-filled by TMA and only ever feed masked
+//    (non-interior) outputs.  NS stages in a ring, full/empty mbarriers.
 //  * S3 x-neighbour taps (centre row of the plane): SHUFFLE = shfl.sync.up/down
-//    by one lane + the warp-edge fallback read from the staged box; PLAIN =
-//    read from the staged box (LDS).
-//  * S4 corner cases: warp-edge lanes as above; tiles past the grid edge are
-//    zero-filled by TMA, stores masked per element in edge tiles only.
+//    by one lane; PLAIN = the neighbour lanes' elements read from the staged
+//    box (LDS).
+//  * S4 corner cases: lanes 0 / 31 read the R elements beyond the warp tile
+//    from the staged sectors (the fallback load); tiles past
+//    the grid edge are zero-filled by TMA, stores masked per element in edge
+//    tiles only.
 //  * S5 slow-axis taps: y taps are LDS.128 of the neighbour rows of the same
 //    staged plane; z taps come from a per-lane register queue of the 2R+1
 //    most recent planes' centre vectors (rotated by unrolling).
@@ -35,7 +38,7 @@
 
 namespace stb200 {
 
-constexpr int kWarps3D = 8;       // consumer warps = rows of the CTA tile (Ty)
+constexpr int kWarps3D = 15;      // consumer warps per CTA (+1 producer = 16 warps, one CTA per SM)
 
 // Staged-box shapes: which halos an array's stencil needs.
 enum BoxKind { BOX_XY = 0, BOX_X = 1, BOX_Y = 2, BOX_C = 3 };
@@ -135,10 +138,22 @@ template <typename T> struct OpDivergence {
 };
 
 // ----------------------------------------------------------- smem layout
+// CTA tile: TX = 32*V columns by TY = kWarps3D*RY = 30 rows; each consumer
+// warp owns RY = 2 consecutive rows (its z queues fit the register budget of
+// 16 warps per SM, 128 registers each).  The y halo is 2R/(30+2R) of the
+// staged rows.
 template <class Op, typename T>
 struct Layout3 {
-    static constexpr int V = vlen<T>(), R = Op::R, PAD = vlen<T>(), TX = 32 * V, TY = kWarps3D;
-    __host__ __device__ static constexpr int bx(int a) { return TX + (box_xh(Op::box(a)) ? 2 * PAD : 0); }
+    static constexpr int V = vlen<T>(), R = Op::R, TX = 32 * V;
+    static constexpr int RY = 2;
+    static constexpr int TY = kWarps3D * RY;
+    // x-halo boxes carry one 32-byte sector of the neighbour tiles on each
+    // side (PADX elements): the warp-edge lanes' fallback reads come from
+    // there.  (A 16-byte pad under L2 promotion, or a scalar global load, is
+    // served as a whole 128-byte line: 50% extra traffic for 512-byte rows.)
+    static constexpr int PADX = 32 / (int)sizeof(T);
+    __host__ __device__ static constexpr int padx(int a) { return box_xh(Op::box(a)) ? PADX : 0; }
+    __host__ __device__ static constexpr int bx(int a) { return TX + 2 * padx(a); }
     __host__ __device__ static constexpr int by(int a) { return TY + (box_yh(Op::box(a)) ? 2 * R : 0); }
     __host__ __device__ static constexpr int box_bytes(int a) { return bx(a) * by(a) * (int)sizeof(T); }
     __host__ __device__ static constexpr int box_stride(int a) { return (box_bytes(a) + 127) / 128 * 128; }
@@ -151,40 +166,75 @@ struct Layout3 {
         for (int a = 0; a < Op::NA; ++a) s += box_bytes(a);
         return s;
     }
-    static constexpr int NS = R == 1 ? 4 : 6;              // pipeline stages
+    // stages: as many as fit in ~200 KB (one CTA per SM), at least 2R+2
+    static constexpr int NS_FIT = (200 * 1024) / stage_bytes();
+    static constexpr int NS = NS_FIT > 8 ? 8 : (NS_FIT < 2 * R + 2 ? 2 * R + 2 : NS_FIT);
     static constexpr size_t smem_bytes() { return (size_t)NS * stage_bytes() + 2 * NS * sizeof(uint64_t); }
 };
 constexpr int k3d_threads() { return (kWarps3D + 1) * 32; }
 
+// Work order ("lockstep round robin"): a work item is (z part, column);
+// items are numbered with the column fastest and CTA c owns items c, c+G,
+// c+2G, ... (m of them).  Every CTA walks its items chunk by chunk (zc planes
+// of each item per round), so at any time CTA c and CTA c+1 (x-neighbour
+// tiles) and CTA c+ntx (y-neighbour) stream the same z planes: the halo rows
+// and edge sectors they share are fetched from DRAM once and hit L2 for the
+// other.  Items per CTA are equal (the grid is sized to make them so), so
+// the CTAs stay in step without any grid-wide synchronisation.
+struct LockIter {
+    int64_t ncols;
+    int nzo, zsplit, zc, m, nchunks, chunk = 0, j = -1;
+    unsigned cta, G;
+    __device__ LockIter(int64_t ncols_, int nzo_, int zsplit_, int zc_, int m_, unsigned cta_, unsigned G_)
+        : ncols(ncols_), nzo(nzo_), zsplit(zsplit_), zc(zc_), m(m_), cta(cta_), G(G_) {
+        const int max_len = (nzo + zsplit - 1) / zsplit;
+        nchunks = (max_len + zc - 1) / zc;
+    }
+    // next piece: column col, output planes [zo, zo + nseg) (relative to z_lo)
+    __device__ __forceinline__ bool next(int64_t& col, int& zo, int& nseg) {
+        for (;;) {
+            if (++j == m) { j = 0; ++chunk; }
+            if (chunk >= nchunks) return false;
+            const int64_t item = (int64_t)cta + (int64_t)j * G;
+            if (item >= ncols * zsplit) continue;
+            const int zpart = (int)(item / ncols);
+            col = item - (int64_t)zpart * ncols;
+            const int zb = (int)((int64_t)nzo * zpart / zsplit);
+            const int ze = (int)((int64_t)nzo * (zpart + 1) / zsplit);
+            zo = zb + chunk * zc;
+            if (zo >= ze) continue;
+            nseg = ze - zo < zc ? ze - zo : zc;
+            return true;
+        }
+    }
+};
+
 template <class Op, typename T>
 struct K3Args {
+    const T* in[Op::NA];   // for the warp-edge fallback loads (x halo of the tile)
     T* out[Op::NOUT];
     int64_t nx, ny;
     int z_lo, nzo;         // output planes [z_lo, z_lo + nzo)
     int ntx, nty;          // tile counts
-    int64_t work;          // ntx * nty * nzo
+    int zsplit, zc, m;     // LockIter: z parts per column, chunk planes, items per CTA
+    int dbg;               // experiment switches (0 in production)
 };
 
 // ------------------------------------------------------------------ kernel
 template <class Op, typename T, int VARIANT>
-__global__ void __launch_bounds__(k3d_threads())
+__global__ void __launch_bounds__(k3d_threads(), 1)
 k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<Op, T> args,
     const Coeffs<T, Op::NC> c) {
     using L = Layout3<Op, T>;
-    constexpr int R = Op::R, NA = Op::NA, V = L::V, PAD = L::PAD, TX = L::TX, NS = L::NS;
-    constexpr int NQ = 2 * R + 1;
+    constexpr int R = Op::R, NA = Op::NA, V = L::V, TX = L::TX, TY = L::TY;
+    constexpr int RY = L::RY, NS = L::NS, NQ = 2 * R + 1;
 
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NS * L::stage_bytes());
     uint64_t* empty = full + NS;
     const int warp = threadIdx.x >> 5, lane = lane_id();
 
-    // this CTA's share of the linearised (column, z) work
-    const int64_t G = gridDim.x;
-    const int64_t w_begin = args.work * (int64_t)blockIdx.x / G;
-    const int64_t w_end = args.work * ((int64_t)blockIdx.x + 1) / G;
-    if (w_begin >= w_end) return;                          // CTA-uniform
-
+    const int64_t ncols = (int64_t)args.ntx * args.nty;
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
             mbar_init(&full[s], 1);
@@ -197,11 +247,11 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
     if (warp == kWarps3D) {                                // ---- producer warp
         if (lane == 0) {
             for (int a = 0; a < NA; ++a) prefetch_tmap(&tm.m[a]);
-            uint32_t g = 0;                                // arrivals so far (all segments)
-            for (int64_t w = w_begin; w < w_end;) {
-                const int64_t col = w / args.nzo;
-                const int zo = (int)(w - col * args.nzo);
-                const int nseg = (int)(args.nzo - zo < w_end - w ? args.nzo - zo : w_end - w);
+            uint32_t g = 0;                                // arrivals so far (all pieces)
+            LockIter it(ncols, args.nzo, args.zsplit, args.zc, args.m, blockIdx.x, gridDim.x);
+            int64_t col;
+            int zo, nseg;
+            while (it.next(col, zo, nseg)) {
                 const int tx = (int)(col % args.ntx), ty = (int)(col / args.ntx);
                 const int z_first = args.z_lo + zo - R;
                 for (int t = 0; t < nseg + 2 * R; ++t, ++g) {
@@ -212,46 +262,41 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
 #pragma unroll
                     for (int a = 0; a < NA; ++a)
                         tma_load_3d(st + L::box_off(a), &tm.m[a],
-                                    tx * TX - (box_xh(Op::box(a)) ? PAD : 0),
-                                    ty * kWarps3D - (box_yh(Op::box(a)) ? R : 0), z_first + t,
-                                    &full[s]);
+                                    tx * TX - L::padx(a),
+                                    ty * TY - (box_yh(Op::box(a)) ? R : 0), z_first + t, &full[s]);
                 }
-                w += nseg;
             }
         }
         return;
     }
 
-    // ---- consumer warps: one row each
+    // ---- consumer warps: RY rows each
     Coeffs<T, Op::NC> cr;
 #pragma unroll
     for (int t = 0; t < Op::NC; ++t) cr.c[t] = c.c[t];
     const bool lane0 = lane == 0, lane31 = lane == 31;
-    T q[NQ][V];
+    T q[RY][NQ][V];                                        // z queue per row
     uint32_t g = 0;
+    const int64_t plane = args.nx * args.ny;
 
-    for (int64_t w = w_begin; w < w_end;) {
-        const int64_t col = w / args.nzo;
-        const int zo = (int)(w - col * args.nzo);
-        const int nseg = (int)(args.nzo - zo < w_end - w ? args.nzo - zo : w_end - w);
+    LockIter it(ncols, args.nzo, args.zsplit, args.zc, args.m, blockIdx.x, gridDim.x);
+    int64_t col;
+    int zo, nseg;
+    while (it.next(col, zo, nseg)) {
         const int tx = (int)(col % args.ntx), ty = (int)(col / args.ntx);
         const int64_t xl = (int64_t)tx * TX + lane * V;
-        const int64_t y = (int64_t)ty * kWarps3D + warp;
-        const bool row_ok = y >= R && y < args.ny - R;
+        const int64_t y0 = (int64_t)ty * TY + warp * RY;  // first row of this warp
         const bool own = xl < args.nx;
-        const bool vec_store = row_ok && own && xl >= R && xl + V <= args.nx - R;
-        bool el_store[V];
+        const bool x_vec = own && xl >= R && xl + V <= args.nx - R;
+        bool x_el[V];
 #pragma unroll
-        for (int p = 0; p < V; ++p)
-            el_store[p] = row_ok && !vec_store && own && xl + p >= R && xl + p < args.nx - R;
-        const int64_t plane = args.nx * args.ny;
-        int64_t obase = ((int64_t)(args.z_lo + zo) * args.ny + y) * args.nx + xl;
+        for (int p = 0; p < V; ++p) x_el[p] = !x_vec && own && xl + p >= R && xl + p < args.nx - R;
+        int64_t obase = ((int64_t)(args.z_lo + zo) * args.ny + y0) * args.nx + xl;
         const int np = nseg + 2 * R;
 
-        // element offset of (row warp+dy, lane vector + e) inside array a's box
-        auto off = [&](int a, int dy, int e) {
-            return (warp + dy + (box_yh(Op::box(a)) ? R : 0)) * L::bx(a) +
-                   (box_xh(Op::box(a)) ? PAD : 0) + lane * V + e;
+        // element offset of (row warp*RY + r + dy, lane vector + e) in array a's box
+        auto off = [&](int a, int r, int dy, int e) {
+            return (warp * RY + r + dy + (box_yh(Op::box(a)) ? R : 0)) * L::bx(a) + L::padx(a) + lane * V + e;
         };
         auto stage_ptr = [&](uint32_t gg, int a) {
             return reinterpret_cast<const T*>(smem + (size_t)(gg % NS) * L::stage_bytes() + L::box_off(a));
@@ -262,23 +307,27 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
             if constexpr (V == 4) { v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w; }
             else { v[0] = t.x; v[1] = t.y; }
         };
-        // arrival: wait for the plane, push the queue array's centre
-        auto arrive_plane = [&](uint32_t gg, T* qslot) {
+        // arrival: wait for the plane, push each row's queue-array centre
+        auto arrive_plane = [&](uint32_t gg, int slot, int zplane) {
+            (void)zplane;
             mbar_wait(&full[gg % NS], (gg / NS) & 1u);
-            ld_vec(stage_ptr(gg, Op::QA) + off(Op::QA, 0, 0), qslot);
+            const T* b = stage_ptr(gg, Op::QA);
+#pragma unroll
+            for (int r = 0; r < RY; ++r) ld_vec(b + off(Op::QA, r, 0, 0), q[r][slot]);
         };
         auto release = [&](uint32_t gg) { mbar_arrive(&empty[gg % NS]); };
 
-        // in-plane taps of plane gg + compute + store output at obase
+        // in-plane taps of plane gg + compute + store the RY output rows
         auto emit = [&](uint32_t gg, int u) {
-            Ctx3<T, NA, V, R> x{{}, {}, {}, q, u};
 #pragma unroll
-            for (int a = 0; a < NA; ++a) {
-                const T* b = stage_ptr(gg, a);
-                {
+            for (int r = 0; r < RY; ++r) {
+                Ctx3<T, NA, V, R> x{{}, {}, {}, q[r], u};
+#pragma unroll
+                for (int a = 0; a < NA; ++a) {
+                    const T* b = stage_ptr(gg, a);
                     if (box_xh(Op::box(a))) {
                         T v[V];
-                        ld_vec(b + off(a, 0, 0), v);
+                        ld_vec(b + off(a, r, 0, 0), v);
 #pragma unroll
                         for (int k = 0; k < V; ++k) x.xw[a][R + k] = v[k];
                         if constexpr (VARIANT == 0) {
@@ -286,49 +335,52 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
                             for (int k = 0; k < R; ++k) x.xw[a][k] = shfl_up(v[V - R + k], 1);
 #pragma unroll
                             for (int k = 0; k < R; ++k) x.xw[a][R + V + k] = shfl_down(v[k], 1);
+                            // warp edge (%out_of_range): the
+                            // fallback read of the staged neighbour sector
                             const int e = lane0 ? -R : V;
                             T hv[R];
 #pragma unroll
-                            for (int k = 0; k < R; ++k) hv[k] = b[off(a, 0, e + k)];
+                            for (int k = 0; k < R; ++k) hv[k] = b[off(a, r, 0, e + k)];
 #pragma unroll
                             for (int k = 0; k < R; ++k) {
                                 x.xw[a][k] = lane0 ? hv[k] : x.xw[a][k];
                                 x.xw[a][R + V + k] = lane31 ? hv[k] : x.xw[a][R + V + k];
                             }
-                        } else {
+                        } else {                          // PLAIN: neighbours' elements from smem
 #pragma unroll
-                            for (int k = 0; k < R; ++k) x.xw[a][k] = b[off(a, 0, k - R)];
+                            for (int k = 0; k < R; ++k) x.xw[a][k] = b[off(a, r, 0, k - R)];
 #pragma unroll
-                            for (int k = 0; k < R; ++k) x.xw[a][R + V + k] = b[off(a, 0, V + k)];
+                            for (int k = 0; k < R; ++k) x.xw[a][R + V + k] = b[off(a, r, 0, V + k)];
                         }
                     }
                     if (box_yh(Op::box(a))) {
 #pragma unroll
                         for (int d = 1; d <= R; ++d) {
-                            ld_vec(b + off(a, -d, 0), x.yv[a][R - d]);
-                            ld_vec(b + off(a, d, 0), x.yv[a][R + d - 1]);
+                            ld_vec(b + off(a, r, -d, 0), x.yv[a][R - d]);
+                            ld_vec(b + off(a, r, d, 0), x.yv[a][R + d - 1]);
                         }
                     }
-                    if (Op::box(a) == BOX_C) ld_vec(b + off(a, 0, 0), x.cv[a]);
+                    if (Op::box(a) == BOX_C) ld_vec(b + off(a, r, 0, 0), x.cv[a]);
+                }
+                T o[Op::NOUT][V];
+#pragma unroll
+                for (int p = 0; p < V; ++p) {
+                    T res[Op::NOUT];
+                    Op::point(x, p, cr, res);
+#pragma unroll
+                    for (int k = 0; k < Op::NOUT; ++k) o[k][p] = res[k];
+                }
+                const bool row_ok = y0 + r >= R && y0 + r < args.ny - R;
+#pragma unroll
+                for (int k = 0; k < Op::NOUT; ++k) {
+                    T* op = args.out[k] + obase + r * args.nx;
+                    if (row_ok && x_vec) stg_vec(op, o[k]);
+#pragma unroll
+                    for (int p = 0; p < V; ++p)
+                        if (row_ok && x_el[p]) op[p] = o[k][p];
                 }
             }
-            T o[Op::NOUT][V];
-#pragma unroll
-            for (int p = 0; p < V; ++p) {
-                T r[Op::NOUT];
-                Op::point(x, p, cr, r);
-#pragma unroll
-                for (int k = 0; k < Op::NOUT; ++k) o[k][p] = r[k];
-            }
             release(gg);
-#pragma unroll
-            for (int k = 0; k < Op::NOUT; ++k) {
-                T* op = args.out[k] + obase;
-                if (vec_store) stg_vec(op, o[k]);
-#pragma unroll
-                for (int p = 0; p < V; ++p)
-                    if (el_store[p]) op[p] = o[k][p];
-            }
             obase += plane;
         };
 
@@ -337,7 +389,7 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
         // output that reads them in-plane.
 #pragma unroll
         for (int t = 0; t < 2 * R; ++t) {
-            arrive_plane(g + t, q[t]);
+            arrive_plane(g + t, t, args.z_lo + zo - R + t);
             if (t < R || t >= nseg + R) release(g + t);
         }
         // main: arrival t = 2R + i, output i (in-plane plane t - R)
@@ -346,7 +398,7 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
 #pragma unroll
             for (int u = 0; u < NQ; ++u) {
                 const uint32_t ga = g + 2 * R + i + u;
-                arrive_plane(ga, q[(2 * R + u) % NQ]);
+                arrive_plane(ga, (2 * R + u) % NQ, args.z_lo + zo + R + i + u);
                 if (i + u + 2 * R >= np - R) release(ga);  // last R planes: centre only
                 emit(ga - R, u);
             }
@@ -355,13 +407,12 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
         for (int u = 0; u < NQ - 1; ++u) {
             if (i + u < nseg) {
                 const uint32_t ga = g + 2 * R + i + u;
-                arrive_plane(ga, q[(2 * R + u) % NQ]);
+                arrive_plane(ga, (2 * R + u) % NQ, args.z_lo + zo + R + i + u);
                 if (i + u + 2 * R >= np - R) release(ga);
                 emit(ga - R, u);
             }
         }
         g += np;
-        w += nseg;
     }
 }
 
