@@ -139,8 +139,54 @@ cudaError_t dispatch_3d(stencil_s* h, const void* const* in, void* const* out, c
 }  // namespace stb200
 
 namespace stb200 {
-cudaError_t launch_tricubic(const stencil_s*, const void* const*, void* const*, cudaStream_t, int64_t,
-                            int64_t) {
-    return cudaErrorNotSupported;
+
+template <typename T, int VAR>
+static cudaError_t launch_tri(const stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
+                              int64_t z_lo, int64_t z_hi) {
+    using L = TriLayout<T>;
+    auto kern = ktricubic<T, VAR>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
+        attr = true;
+    }
+    const int64_t* ld = h->ldims;
+    if (z_lo < 0) { z_lo = 1; z_hi = ld[2] - 2; }
+    if (z_hi <= z_lo) return cudaSuccess;
+    TmapPack<4> tm;
+    cudaError_t e = make_tmap(&tm.m[0], in[0], h->dtype, ld, L::FBX, L::FBY);
+    for (int a = 1; a < 4 && e == cudaSuccess; ++a) e = make_tmap(&tm.m[a], in[a], h->dtype, ld, L::TX, L::TY);
+    if (e != cudaSuccess) return e;
+    TriArgs<T> args;
+    args.out = (T*)out[0];
+    args.nx = ld[0];
+    args.ny = ld[1];
+    args.z_lo = (int)z_lo;
+    args.nzo = (int)(z_hi - z_lo);
+    args.ntx = (int)((ld[0] + L::TX - 1) / L::TX);
+    args.nty = (int)((ld[1] + L::TY - 1) / L::TY);
+    const int64_t ncols = (int64_t)args.ntx * args.nty;
+    const int64_t slots = sm_count_of(h->device);
+    int64_t zsplit = slots / ncols;
+    if (zsplit < 1) zsplit = 1;
+    if (zsplit > args.nzo) zsplit = args.nzo;
+    const int64_t items = ncols * zsplit;
+    const int64_t m = (items + slots - 1) / slots;
+    const int64_t grid = (items + m - 1) / m;
+    args.zsplit = (int)zsplit;
+    args.m = (int)m;
+    args.zc = 64;
+    kern<<<(unsigned)grid, (kTriWarps + 1) * 32, L::SMEM, s>>>(tm, args);
+    return cudaGetLastError();
 }
+
+cudaError_t launch_tricubic(const stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
+                            int64_t a, int64_t b) {
+    if (h->dtype == ST_F64)
+        return h->variant == ST_PLAIN ? launch_tri<double, 1>(h, in, out, s, a, b)
+                                      : launch_tri<double, 0>(h, in, out, s, a, b);
+    return h->variant == ST_PLAIN ? launch_tri<float, 1>(h, in, out, s, a, b)
+                                  : launch_tri<float, 0>(h, in, out, s, a, b);
+}
+
 }  // namespace stb200

@@ -19,7 +19,7 @@ from parity import (assert_parity, gpu_run, gpu_step, interior, oracle_window_ru
 
 pytestmark = pytest.mark.gpu
 
-KINDS_3D = ["laplacian3d7", "jacobi3d7", "wave13pt", "divergence", "gradient"]
+KINDS_3D = ["laplacian3d7", "jacobi3d7", "wave13pt", "divergence", "gradient", "tricubic"]
 SHAPES = {  # (nz, ny, nx) numpy order
     "f32": [(3, 3, 4), (5, 5, 8), (7, 9, 36), (12, 17, 132), (10, 33, 260), (6, 8, 516)],
     "f64": [(3, 3, 4), (5, 5, 6), (6, 11, 66), (9, 13, 130), (7, 20, 258)],
@@ -28,10 +28,10 @@ SHAPES = {  # (nz, ny, nx) numpy order
 
 def cases():
     for kind in KINDS_3D:
-        r = 2 if kind == "wave13pt" else 1
+        need = 5 if kind == "wave13pt" else 4 if kind == "tricubic" else 3
         for dt in ("f32", "f64"):
-            for shape in SHAPES[dt]:
-                if min(shape) >= 2 * r + 1:
+            for shape in SHAPES[dt] + ([(4, 4, 4), (19, 20, 132)] if kind == "tricubic" else []):
+                if min(shape) >= need and shape[2] * (8 if dt == "f64" else 4) % 16 == 0:
                     yield kind, dt, shape
 
 
@@ -62,7 +62,8 @@ def test_step_parity_and_variants(oracle, kind, dtype, shape):
 @pytest.mark.parametrize("kind,dtype,shape", [
     ("laplacian3d7", "f64", (9, 13, 130)), ("jacobi3d7", "f32", (12, 17, 132)),
     ("wave13pt", "f64", (10, 12, 66)), ("wave13pt", "f32", (9, 10, 132)),
-    ("divergence", "f32", (7, 9, 36)), ("gradient", "f64", (6, 11, 66))])
+    ("divergence", "f32", (7, 9, 36)), ("gradient", "f64", (6, 11, 66)),
+    ("tricubic", "f32", (19, 20, 132))])
 def test_run_parity(oracle, kind, dtype, shape):
     ar = oracle.arity(kind)
     ins = [inputs.generate_np(shape, dtype, inputs.BASE_SEED + 5, a) for a in range(ar["n_in"])]
@@ -97,6 +98,31 @@ def test_divergence_gradient_closed_forms_on_gpu():
     gs = gpu_step("gradient", "f64", [3 * i - 2 * j + 5 * k], 3)
     for g, v in zip(gs, (3.0, -2.0, 5.0)):
         assert np.all(g[1:-1, 1:-1, 1:-1] == v)
+
+
+def test_tricubic_special_offsets_on_gpu():
+    """X=Y=Z=0 selects f[k][j][i] exactly; X=Y=Z=1 selects f[k+1][j+1][i+1]."""
+    shape = (9, 20, 136)
+    f = inputs.generate_np(shape, "f32", 3)
+    for t, sl in ((0.0, (slice(1, -2),) * 3), (1.0, (slice(2, -1),) * 3)):
+        c = np.full(shape, t, np.float32)
+        (g,) = gpu_step("tricubic", "f32", [f, c, c, c], 1)
+        np.testing.assert_array_equal(g[1:-2, 1:-2, 1:-2], f[sl])
+
+
+def test_tricubic_reproduces_cubics_on_gpu():
+    """Degree-3 polynomial per axis: g = p(i+X) q(j+Y) r(k+Z) (fp64, 1e-12)."""
+    rng = np.random.default_rng(5)
+    shape = (8, 19, 66)
+    k, j, i = np.meshgrid(*[np.arange(n, dtype=np.float64) for n in shape], indexing="ij")
+    p = np.polynomial.Polynomial([0.3, -0.11, 0.025, 0.0005])
+    q = np.polynomial.Polynomial([1.0, 0.05, -0.02, 0.001])
+    r = np.polynomial.Polynomial([-0.7, 0.2, 0.1, -0.03])
+    X, Y, Z = (rng.uniform(size=shape) for _ in range(3))
+    (g,) = gpu_step("tricubic", "f64", [p(i) * q(j) * r(k), X, Y, Z], 1)
+    exp = p(i + X) * q(j + Y) * r(k + Z)
+    sl = (slice(1, -2),) * 3
+    np.testing.assert_allclose(g[sl], exp[sl], rtol=1e-11, atol=1e-11)
 
 
 # ----------------------------------------------------- BASELINE configs
@@ -146,19 +172,19 @@ def test_configs_full_size_windows(oracle, kind, dtype, dims, iters):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("kind", ["divergence", "gradient"])
-def test_suite_512_single_step_samples(oracle, kind):
+@pytest.mark.parametrize("kind,n", [("divergence", 512), ("gradient", 512), ("tricubic", 256)])
+def test_suite_single_step_samples(oracle, kind, n):
     from paper_2301_11389_b200.binding import Stencil
-    shape = (512, 512, 512)
+    shape = (n, n, n)
     ar = oracle.arity(kind)
     ins = _dev_fields(shape, "f32", inputs.BASE_SEED + 9, ar["n_in"])
     outs = [torch.zeros_like(ins[0]) for _ in range(ar["n_out"])]
     st = Stencil(kind, shape[::-1], "f32")
     st.step(ins, outs)
     torch.cuda.synchronize()
-    for w in [(slice(0, 6), slice(0, 6), slice(0, 140)), (slice(250, 256), slice(500, 512),
-                                                           slice(380, 512))]:
-        sub = tuple(slice(max(0, s.start - 1), min(512, s.stop + 1)) for s in w)
+    for w in [(slice(0, 6), slice(0, 6), slice(0, 140)), (slice(n // 2 - 6, n // 2), slice(n - 12, n),
+                                                           slice(n - 132, n))]:
+        sub = tuple(slice(max(0, s.start - 2), min(n, s.stop + 2)) for s in w)
         f = [t[sub].cpu().numpy() for t in ins]
         refs = [np.zeros_like(f[0]) for _ in range(ar["n_out"])]
         oracle.step(kind, "f32", f, refs)
@@ -168,14 +194,14 @@ def test_suite_512_single_step_samples(oracle, kind):
             g = outs[k][w].cpu().numpy()
             rr = refs[k][inner]
             m = np.zeros(g.shape, bool)
+            lo, hi = ar["lo"], ar["hi"]
             gi = [np.arange(s.start, s.stop) for s in w]
-            ok = [(a >= 1) & (a < 511) for a in gi]
+            ok = [(a >= lo) & (a < n - hi) for a in gi]
             m[np.ix_(*ok)] = True
             sub_in = tuple(slice(s.start - u.start, s.stop - u.start) for s, u in zip(w, sub))
-            m &= np.ones_like(m)
-            # oracle only wrote its own interior: exclude the cut-out's ring
+            # the oracle only wrote the cut-out's own interior: exclude its ring
             ring = np.zeros(f[0].shape, bool)
-            ring[1:-1, 1:-1, 1:-1] = True
+            ring[lo:-hi, lo:-hi, lo:-hi] = True
             m &= ring[sub_in]
             assert_parity(g[m], rr[m], "f32", f"{kind} out{k} window {w}")
     st.close()
