@@ -153,11 +153,13 @@ static cudaError_t launch_tri(const stencil_s* h, const void* const* in, void* c
     const int64_t* ld = h->ldims;
     if (z_lo < 0) { z_lo = 1; z_hi = ld[2] - 2; }
     if (z_hi <= z_lo) return cudaSuccess;
-    TmapPack<4> tm;
+    TmapPack<1> tm;
     cudaError_t e = make_tmap(&tm.m[0], in[0], h->dtype, ld, L::FBX, L::FBY);
-    for (int a = 1; a < 4 && e == cudaSuccess; ++a) e = make_tmap(&tm.m[a], in[a], h->dtype, ld, L::TX, L::TY);
     if (e != cudaSuccess) return e;
     TriArgs<T> args;
+    args.X = (const T*)in[1];
+    args.Y = (const T*)in[2];
+    args.Z = (const T*)in[3];
     args.out = (T*)out[0];
     args.nx = ld[0];
     args.ny = ld[1];

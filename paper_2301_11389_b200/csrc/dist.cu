@@ -126,8 +126,6 @@ static int nccl_check(ncclResult_t r, const char* what) {
 int dist_step(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s) {
     DistState* d = h->dist;
     NcclApi& api = nccl();
-    const int lo = h->k->lo, hi = h->k->hi;
-    const int64_t m = d->m;
     const size_t pb = d->plane_bytes;
     const bool has_lower = h->rank > 0, has_upper = h->rank < h->nranks - 1;
     cudaError_t e;
@@ -139,16 +137,20 @@ int dist_step(stencil_s* h, const void* const* in, void* const* out, cudaStream_
     int rc;
     if ((rc = nccl_check(api.GroupStart(), "ncclGroupStart"))) return rc;
     const unsigned mask = halo_inputs(h->k->kind);
+    // offsets and counts straight from the host plan (stencil_slab_plan)
+    const int64_t recv_lo_at = d->plan[3], send_lo_from = d->plan[4];
+    const int64_t recv_hi_at = d->plan[5], send_hi_from = d->plan[6];
+    const size_t n_lo = (size_t)(d->plan[7] & 0xFFFF), n_hi = (size_t)(d->plan[7] >> 16);
     for (int a = 0; a < h->k->n_in; ++a) {
         if (!(mask >> a & 1u)) continue;
         char* buf = (char*)in[a];      // the halo planes of an input are the exchange's
-        if (has_lower) {
-            api.Send(buf + (size_t)lo * pb, (size_t)hi * pb, kNcclInt8, h->rank - 1, d->comm, d->comm_stream);
-            api.Recv(buf, (size_t)lo * pb, kNcclInt8, h->rank - 1, d->comm, d->comm_stream);
+        if (has_lower) {               // my bottom hi owned planes <-> rank-1's top lo planes
+            api.Send(buf + (size_t)send_lo_from * pb, n_hi * pb, kNcclInt8, h->rank - 1, d->comm, d->comm_stream);
+            api.Recv(buf + (size_t)recv_lo_at * pb, n_lo * pb, kNcclInt8, h->rank - 1, d->comm, d->comm_stream);
         }
-        if (has_upper) {
-            api.Send(buf + (size_t)m * pb, (size_t)lo * pb, kNcclInt8, h->rank + 1, d->comm, d->comm_stream);
-            api.Recv(buf + (size_t)(lo + m) * pb, (size_t)hi * pb, kNcclInt8, h->rank + 1, d->comm,
+        if (has_upper) {               // my top lo owned planes <-> rank+1's bottom hi planes
+            api.Send(buf + (size_t)send_hi_from * pb, n_lo * pb, kNcclInt8, h->rank + 1, d->comm, d->comm_stream);
+            api.Recv(buf + (size_t)recv_hi_at * pb, n_hi * pb, kNcclInt8, h->rank + 1, d->comm,
                      d->comm_stream);
         }
     }

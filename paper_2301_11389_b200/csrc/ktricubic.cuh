@@ -12,8 +12,10 @@
 //
 //  * S1/S2: one CTA per SM, kTriWarps consumer warps (one output row each)
 //    + 1 producer warp; per z-plane one TMA box of f ((128+16) x (TY+3):
-//    one 32-byte sector each side for the x halo, rows j-1..j+2) and three
-//    centre boxes (X, Y, Z); lockstep round-robin work order (LockIter).
+//    one 32-byte sector each side for the x halo, rows j-1..j+2) into an
+//    8-stage ring; the offsets X, Y, Z (read once, no neighbours) are
+//    LDG.128 loads issued one output plane ahead; lockstep round-robin work
+//    order (LockIter).
 //  * S3/S4: per f row, each lane holds its 4 points plus 1 element on the
 //    left and 2 on the right: SHUFFLE = shfl.up by 1 / shfl.down by 1 (two
 //    values), warp-edge lanes read the staged pad sectors; PLAIN = LDS.
@@ -32,6 +34,7 @@ constexpr int kTriWarps = 15;     // consumer warps (+1 producer = 16 warps, one
 
 // Two-point arithmetic: packed FFMA2/FMUL2/FADD2 for fp32, DFMA pairs for fp64.
 template <typename T> struct P2;
+#ifndef STB200_TRI_SCALAR
 template <> struct P2<float> {
     using t = float2;
     __device__ static t mk(float a, float b) { return make_float2(a, b); }
@@ -40,6 +43,16 @@ template <> struct P2<float> {
     __device__ static t add(t a, t b) { return __fadd2_rn(a, b); }
     __device__ static t sub(t a, t b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
 };
+#else
+template <> struct P2<float> {
+    using t = float2;
+    __device__ static t mk(float a, float b) { return make_float2(a, b); }
+    __device__ static t mul(t a, t b) { return make_float2(a.x * b.x, a.y * b.y); }
+    __device__ static t fma(t a, t b, t c) { return make_float2(fmaf(a.x, b.x, c.x), fmaf(a.y, b.y, c.y)); }
+    __device__ static t add(t a, t b) { return make_float2(a.x + b.x, a.y + b.y); }
+    __device__ static t sub(t a, t b) { return make_float2(a.x - b.x, a.y - b.y); }
+};
+#endif
 template <> struct P2<double> {
     using t = double2;
     __device__ static t mk(double a, double b) { return make_double2(a, b); }
@@ -54,18 +67,17 @@ struct TriLayout {
     static constexpr int ES = (int)sizeof(T), V = 16 / ES, TX = 32 * V, TY = kTriWarps, PADX = 32 / ES;
     static constexpr int FBX = TX + 2 * PADX, FBY = TY + 3;     // f box
     static constexpr int F_BYTES = FBX * FBY * ES;
-    static constexpr int C_BYTES = TX * TY * ES;                // X / Y / Z boxes
-    static constexpr int F_STRIDE = (F_BYTES + 127) / 128 * 128;
-    static constexpr int C_STRIDE = (C_BYTES + 127) / 128 * 128;
-    static constexpr int STAGE = F_STRIDE + 3 * C_STRIDE;
-    static constexpr int TX_BYTES = F_BYTES + 3 * C_BYTES;
-    static constexpr int NS = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;   // >= 4 in use + prefetch
+    static constexpr int STAGE = (F_BYTES + 127) / 128 * 128;
+    static constexpr int TX_BYTES = F_BYTES;
+    static constexpr int NS = 8;                                // 4 planes in use + 4 in flight
     static constexpr size_t SMEM = (size_t)NS * STAGE + 2 * NS * sizeof(uint64_t);
-    static_assert(NS >= 5, "tricubic needs 4 staged planes plus prefetch");
 };
 
 template <typename T>
 struct TriArgs {
+    const T* X;            // per-point offsets: read with LDG.128, one output plane ahead
+    const T* Y;
+    const T* Z;
     T* out;
     int64_t nx, ny;
     int z_lo, nzo, ntx, nty, zsplit, zc, m;
@@ -90,7 +102,7 @@ __device__ __forceinline__ void lagrange4x2(typename P2<T>::t t, typename P2<T>:
 
 template <typename T, int VARIANT>
 __global__ void __launch_bounds__((kTriWarps + 1) * 32, 1)
-ktricubic(const __grid_constant__ TmapPack<4> tm, const __grid_constant__ TriArgs<T> args) {
+ktricubic(const __grid_constant__ TmapPack<1> tm, const __grid_constant__ TriArgs<T> args) {
     using L = TriLayout<T>;
     using P = P2<T>;
     using T2 = typename P::t;
@@ -112,7 +124,7 @@ ktricubic(const __grid_constant__ TmapPack<4> tm, const __grid_constant__ TriArg
 
     if (warp == kTriWarps) {                               // ---- producer warp
         if (lane == 0) {
-            for (int a = 0; a < 4; ++a) prefetch_tmap(&tm.m[a]);
+            prefetch_tmap(&tm.m[0]);
             uint32_t g = 0;
             LockIter it(ncols, args.nzo, args.zsplit, args.zc, args.m, blockIdx.x, gridDim.x);
             int64_t col;
@@ -124,11 +136,8 @@ ktricubic(const __grid_constant__ TmapPack<4> tm, const __grid_constant__ TriArg
                     const uint32_t s = g % NS;
                     if (g >= NS) mbar_wait(&empty[s], (g / NS - 1) & 1u);
                     mbar_arrive_expect_tx(&full[s], L::TX_BYTES);
-                    unsigned char* st = smem + (size_t)s * L::STAGE;
-                    tma_load_3d(st, &tm.m[0], tx * TX - PADX, ty * TY - 1, z_first + t, &full[s]);
-                    for (int a = 1; a < 4; ++a)
-                        tma_load_3d(st + L::F_STRIDE + (a - 1) * L::C_STRIDE, &tm.m[a], tx * TX, ty * TY,
-                                    z_first + t, &full[s]);
+                    tma_load_3d(smem + (size_t)s * L::STAGE, &tm.m[0], tx * TX - PADX, ty * TY - 1,
+                                z_first + t, &full[s]);
                 }
             }
         }
@@ -163,20 +172,33 @@ ktricubic(const __grid_constant__ TmapPack<4> tm, const __grid_constant__ TriArg
             else { v[0] = t.x; v[1] = t.y; }
         };
 
+        // offsets of the first output plane; later planes are fetched one
+        // plane ahead (clamped address past the grid: values unused)
+        const int64_t xoff = (y < args.ny ? y : args.ny - 1) * args.nx + (own ? xl : args.nx - V);
+        const T* px = args.X + (int64_t)(args.z_lo + zo) * plane + xoff;
+        const T* py = args.Y + (int64_t)(args.z_lo + zo) * plane + xoff;
+        const T* pz = args.Z + (int64_t)(args.z_lo + zo) * plane + xoff;
+        T Xn[V], Yn[V], Zn[V];
+        ldg_vec(Xn, px);
+        ldg_vec(Yn, py);
+        ldg_vec(Zn, pz);
         wait(g);
         wait(g + 1);
         wait(g + 2);
         for (int o = 0; o < nseg; ++o) {
+            T X[V], Y[V], Z[V];
+#pragma unroll
+            for (int p = 0; p < V; ++p) { X[p] = Xn[p]; Y[p] = Yn[p]; Z[p] = Zn[p]; }
+            if (o + 1 < nseg) {
+                px += plane; py += plane; pz += plane;
+                ldg_vec(Xn, px);
+                ldg_vec(Yn, py);
+                ldg_vec(Zn, pz);
+            }
             wait(g + o + 3);
-            // weights of the V points from X, Y, Z at this output plane (arrival o+1)
+            // weights of the V points from their offsets X, Y, Z
             T2 wx[NP][4], wy[NP][4], wz[NP][4];
             {
-                const unsigned char* st = stage(g + o + 1) + L::F_STRIDE;
-                const int e = warp * TX + lane * V;
-                T X[V], Y[V], Z[V];
-                ldv((const T*)st + e, X);
-                ldv((const T*)(st + L::C_STRIDE) + e, Y);
-                ldv((const T*)(st + 2 * L::C_STRIDE) + e, Z);
 #pragma unroll
                 for (int pp = 0; pp < NP; ++pp) {
                     lagrange4x2<T>(P::mk(X[2 * pp], X[2 * pp + 1]), wx[pp]);
