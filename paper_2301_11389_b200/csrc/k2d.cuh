@@ -39,7 +39,7 @@
 namespace stb200 {
 
 constexpr int kWarps2D = 4;       // x-tiles per CTA (128 threads)
-constexpr int kStages2D = 8;      // staged rows per CTA (bulk copies in flight); power of 2
+constexpr int kStages2D = 16;     // staged rows per CTA (bulk copies in flight); power of 2
 
 enum { VAR_SHUFFLE = 0, VAR_PLAIN = 1 };
 
