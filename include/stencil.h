@@ -73,8 +73,23 @@ enum stencil_dtype { ST_F32 = 1, ST_F64 = 2, ST_I32 = 3 };
  *              fall back to a predicated load (the %out_of_range corner case,
  *              PAPER.md:561-564).
  *  ST_PLAIN:   the same taps come from loads (L1 / shared memory), i.e. the
- *              original code's loads, no shuffles. */
-enum stencil_variant { ST_SHUFFLE = 0, ST_PLAIN = 1 };
+ *              original code's loads, no shuffles.
+ * The paper-literal family (2-D kinds, fp32/int32 only: the paper shuffles
+ * 32-bit data): one output per thread, 512 threads per
+ * block along x (Listing 5), leftmost tap of each x-row as
+ * the shuffle source, written as the PTX of Listing 6:
+ *  ST_PAPER_ORIGINAL: every tap an ld.global.nc (the compiler's code)
+ *  ST_PAPER_PTXASW:   activemask / %incomplete / %out_of_range / or.pred,
+ *                     shfl.sync.down at the load site, @pred original load
+ *  ST_PAPER_NOLOAD:   covered loads removed (INVALID results)
+ *  ST_PAPER_NOCORNER: shuffles without corner fallback (INVALID at warp edges)
+ *  ST_PAPER_UNIFORM:  warp-uniform branch on completeness
+ * Bit-identical to SHUFFLE/PLAIN except NOLOAD and NOCORNER. */
+enum stencil_variant {
+    ST_SHUFFLE = 0, ST_PLAIN = 1,
+    ST_PAPER_ORIGINAL = 2, ST_PAPER_PTXASW = 3, ST_PAPER_NOLOAD = 4, ST_PAPER_NOCORNER = 5,
+    ST_PAPER_UNIFORM = 6
+};
 
 enum stencil_status {
     ST_OK = 0,
@@ -94,7 +109,8 @@ enum stencil_status {
 int stencil_create(stencil_t* h, int kind, int ndims, const int64_t* dims, int dtype,
                    const double* coeffs, int ncoeffs);
 
-/* Select ST_SHUFFLE (default) or ST_PLAIN for subsequent calls. */
+/* Select the kernel variant for subsequent calls (default ST_SHUFFLE);
+ * ST_EUNSUPPORTED for a paper-literal variant on a 3-D or fp64 handle. */
 int stencil_set_variant(stencil_t h, int variant);
 int stencil_get_variant(stencil_t h, int* variant);
 

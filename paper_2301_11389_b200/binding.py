@@ -18,7 +18,8 @@ KINDS = {"jacobi2d5": 1, "jacobi2d9": 2, "gaussblur5x5": 3, "gameoflife": 4,
          "laplacian3d7": 5, "jacobi3d7": 6, "wave13pt": 7, "divergence": 8,
          "gradient": 9, "tricubic": 10}
 DTYPES = {"f32": 1, "f64": 2, "i32": 3}
-VARIANTS = {"shuffle": 0, "plain": 1}
+VARIANTS = {"shuffle": 0, "plain": 1, "paper_original": 2, "paper_ptxasw": 3,
+            "paper_noload": 4, "paper_nocorner": 5, "paper_uniform": 6}
 STATUS = {0: "ST_OK", -1: "ST_EARG", -2: "ST_EUNSUPPORTED", -3: "ST_EALIGN",
           -4: "ST_ECUDA", -5: "ST_ENCCL", -6: "ST_ESTATE"}
 

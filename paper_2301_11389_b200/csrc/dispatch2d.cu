@@ -1,6 +1,7 @@
 // dispatch2d.cu — host launchers of the 2-D kernels (k2d.cuh).
 #include "internal.h"
 #include "k2d.cuh"
+#include "kpaper.cuh"
 
 namespace stb200 {
 
@@ -59,9 +60,47 @@ static cudaError_t launch_var(const stencil_s* h, const void* in, void* out, cud
     return launch_k2d<OpT<T>, T, VAR_SHUFFLE>(h, in, out, s, a, b);
 }
 
+// The paper-literal family (kpaper.cuh): one output per thread, 512 threads
+// per block along x, one block row per output row.
+template <typename T, int KIND, int PV>
+static cudaError_t launch_kpaper(const stencil_s* h, const void* in, void* out, cudaStream_t s,
+                                 int64_t y_lo, int64_t y_hi) {
+    constexpr int R = PaperOp<T, KIND>::R;
+    const int64_t nx = h->ldims[0], ny = h->ldims[1];
+    if (y_lo < 0) { y_lo = R; y_hi = ny - R; }
+    if (y_hi <= y_lo) return cudaSuccess;
+    if (y_hi - y_lo > 65535) return cudaErrorInvalidConfiguration;
+    Coeffs<T, PaperOp<T, KIND>::NC> c{};
+    for (int t = 0; t < PaperOp<T, KIND>::NC; ++t) c.c[t] = (T)h->coeffs[t];
+    const dim3 grid((unsigned)((nx - 2 * R + kPaperThreads - 1) / kPaperThreads), (unsigned)(y_hi - y_lo));
+    kpaper<T, KIND, PV><<<grid, kPaperThreads, 0, s>>>((const T*)in, (T*)out, nx, (int)y_lo, c);
+    return cudaGetLastError();
+}
+
+template <typename T, int KIND>
+static cudaError_t paper_var(const stencil_s* h, const void* in, void* out, cudaStream_t s, int64_t a,
+                             int64_t b) {
+    switch (h->variant) {
+    case ST_PAPER_ORIGINAL: return launch_kpaper<T, KIND, PV_ORIGINAL>(h, in, out, s, a, b);
+    case ST_PAPER_PTXASW: return launch_kpaper<T, KIND, PV_PTXASW>(h, in, out, s, a, b);
+    case ST_PAPER_NOLOAD: return launch_kpaper<T, KIND, PV_NOLOAD>(h, in, out, s, a, b);
+    case ST_PAPER_NOCORNER: return launch_kpaper<T, KIND, PV_NOCORNER>(h, in, out, s, a, b);
+    default: return launch_kpaper<T, KIND, PV_UNIFORM>(h, in, out, s, a, b);
+    }
+}
+
 cudaError_t dispatch_2d(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
                         int64_t a, int64_t b) {
     const bool f64 = h->dtype == ST_F64;
+    if (h->variant >= ST_PAPER_ORIGINAL) {                 // validated f32/i32 in set_variant
+        switch (h->k->kind) {
+        case ST_JACOBI2D5: return paper_var<float, 1>(h, in[0], out[0], s, a, b);
+        case ST_JACOBI2D9: return paper_var<float, 2>(h, in[0], out[0], s, a, b);
+        case ST_GAUSSBLUR5X5: return paper_var<float, 3>(h, in[0], out[0], s, a, b);
+        case ST_GAMEOFLIFE: return paper_var<int, 4>(h, in[0], out[0], s, a, b);
+        default: return cudaErrorInvalidValue;
+        }
+    }
     switch (h->k->kind) {
     case ST_JACOBI2D5:
         return f64 ? launch_var<OpJacobi2D5, double>(h, in[0], out[0], s, a, b)
