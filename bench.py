@@ -30,6 +30,7 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("NCCL_DEBUG", "WARN")     # keep stdout to the one JSON line
 
 # name -> kind, dtype, dims at N=1 (x fastest), iterations, weak-scaled axis
 WORKLOADS = {
@@ -226,6 +227,8 @@ def main():
     ap.add_argument("--variant", default="shuffle", choices=["shuffle", "plain"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--attach", action="store_true",
+                    help="run the NCCL-attached (slab) path even at N=1 (a group of one rank)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
@@ -259,6 +262,8 @@ def main():
             uid.copy_(torch.frombuffer(bytearray(dist_get_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
         st.attach(bytes(uid.cpu().tolist()), rank, world)
+    elif args.attach:                 # the multi-GPU code path with a group of one
+        st.attach(dist_get_id(), 0, 1)
     info = st.info()
     n_in, n_out, n_bufs = st.arity()
     ldims = info["local_dims"][: len(dims)]
@@ -380,7 +385,8 @@ def main():
             "dtype": wl["dtype"], "data": "synthetic (splitmix64 seeded grids, DESIGN.md §6)",
             "config": {"workload": wl["config"], "kind": wl["kind"], "dims": dims,
                        "local_dims": list(ldims), "iters_per_step": iters,
-                       "variant": args.variant, "parallelism": f"slab{world}" if world > 1 else "1gpu",
+                       "variant": args.variant,
+                       "parallelism": f"slab{world}" if world > 1 else ("slab1" if args.attach else "1gpu"),
                        "l2": "flushed between timed steps" if flush is not None
                        else "inputs larger than L2"},
             "hbm_gbs": achieved * 1.0,
