@@ -54,6 +54,34 @@ __device__ __forceinline__ void ldg_run(T* v, const T* p) {
     }
 }
 
+// Predicated shared-memory load of R consecutive elements into dst (dst is
+// left unchanged where the predicate is false): the corner-lane fallback
+// without a select.  The address is R*sizeof(T)-aligned at every call site.
+template <typename T, int R>
+__device__ __forceinline__ void lds_pred(bool p, const T* src, T* dst) {
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(src));
+    const int pi = p ? 1 : 0;
+    if constexpr (std::is_same<T, float>::value && R == 2) {
+        asm volatile("{.reg .pred q; setp.ne.b32 q, %2, 0; @q ld.shared.v2.f32 {%0, %1}, [%3];}"
+                     : "+f"(dst[0]), "+f"(dst[1]) : "r"(pi), "r"(a));
+    } else if constexpr (std::is_same<T, float>::value && R == 1) {
+        asm volatile("{.reg .pred q; setp.ne.b32 q, %1, 0; @q ld.shared.f32 %0, [%2];}"
+                     : "+f"(dst[0]) : "r"(pi), "r"(a));
+    } else if constexpr (std::is_same<T, int>::value && R == 2) {
+        asm volatile("{.reg .pred q; setp.ne.b32 q, %2, 0; @q ld.shared.v2.b32 {%0, %1}, [%3];}"
+                     : "+r"(dst[0]), "+r"(dst[1]) : "r"(pi), "r"(a));
+    } else if constexpr (std::is_same<T, int>::value && R == 1) {
+        asm volatile("{.reg .pred q; setp.ne.b32 q, %1, 0; @q ld.shared.b32 %0, [%2];}"
+                     : "+r"(dst[0]) : "r"(pi), "r"(a));
+    } else if constexpr (std::is_same<T, double>::value && R == 2) {
+        asm volatile("{.reg .pred q; setp.ne.b32 q, %2, 0; @q ld.shared.v2.f64 {%0, %1}, [%3];}"
+                     : "+d"(dst[0]), "+d"(dst[1]) : "r"(pi), "r"(a));
+    } else {
+        asm volatile("{.reg .pred q; setp.ne.b32 q, %1, 0; @q ld.shared.f64 %0, [%2];}"
+                     : "+d"(dst[0]) : "r"(pi), "r"(a));
+    }
+}
+
 // Shuffles move 32-bit patterns unchanged (PAPER.md:272-274 restricts the
 // paper to 32-bit data); a 64-bit element is two SHFL.
 __device__ __forceinline__ float  shfl_up(float v, int d)   { return __shfl_up_sync(FULL, v, d); }

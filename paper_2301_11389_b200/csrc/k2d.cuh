@@ -98,7 +98,10 @@ template <typename T> struct OpGauss5 {
         return acc;
     }
     // fp32: two adjacent outputs (p, p+1) per packed FFMA2 (fma.rn.f32x2):
-    // the same per-point FMA chain as point(), half the issue slots.
+    // the same per-point FMA chain as point(), fewer issue slots.  A tap
+    // whose operand pair (w[e], w[e+1]) starts at an even element is one
+    // FFMA2 on an aligned register pair; an odd start would need two moves
+    // to build the pair, so it is issued as two scalar FFMAs instead.
     static constexpr bool kPaired = std::is_same<T, float>::value;
     template <class Wn>
     __device__ __forceinline__ static float2 point2(const Wn& w, int p, const Coeffs<T, NC>& c) {
@@ -106,7 +109,12 @@ template <typename T> struct OpGauss5 {
 #pragma unroll
         for (int t = 1; t < 25; ++t) {
             const int dj = t / 5 - 2, e = p + t % 5;
-            acc = __ffma2_rn(make_float2(c.c[t], c.c[t]), make_float2(w(dj, e), w(dj, e + 1)), acc);
+            if ((e & 1) == 0) {
+                acc = __ffma2_rn(make_float2(c.c[t], c.c[t]), make_float2(w(dj, e), w(dj, e + 1)), acc);
+            } else {
+                acc.x = fmaf(c.c[t], w(dj, e), acc.x);
+                acc.y = fmaf(c.c[t], w(dj, e + 1), acc.y);
+            }
         }
         return acc;
     }
@@ -231,17 +239,10 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
             for (int k = 0; k < R; ++k) dst[k] = shfl_up(v[V - R + k], 1);
 #pragma unroll
             for (int k = 0; k < R; ++k) dst[R + V + k] = shfl_down(v[k], 1);
-            // warp-edge lanes: the fallback load, from the
-            // staged row; a select of two loaded values keeps it branch-free
-            const int e = lane0 ? lo_e - R : lo_e + V;
-            T hv[R];
-#pragma unroll
-            for (int k = 0; k < R; ++k) hv[k] = row[e + k];
-#pragma unroll
-            for (int k = 0; k < R; ++k) {
-                dst[k] = lane0 ? hv[k] : dst[k];
-                dst[R + V + k] = lane31 ? hv[k] : dst[R + V + k];
-            }
+            // warp-edge lanes: the fallback load from the
+            // staged row, predicated on %out_of_range (no branch, no select)
+            lds_pred<T, R>(lane0, row + lo_e - R, dst);
+            lds_pred<T, R>(lane31, row + lo_e + V, dst + R + V);
         } else {
 #pragma unroll
             for (int k = 0; k < R; ++k) dst[k] = row[lo_e - R + k];
@@ -271,7 +272,6 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
         auto emit = [&](int u) {
             T o[V];
             const Win<T, NW, W, R> w{win, u};
-#pragma unroll
             if constexpr (HasPaired<Op>::value) {                       // S6
 #pragma unroll
                 for (int p = 0; p < V; p += 2) {
