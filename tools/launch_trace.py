@@ -9,16 +9,21 @@ import bench
 wl = bench.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "gaussblur"]
 var = sys.argv[2] if len(sys.argv) > 2 else "shuffle"
 st = Stencil(wl["kind"], wl["dims"], wl["dtype"], variant=var)
-a = inputs.generate_torch(tuple(wl["dims"][::-1]), wl["dtype"], 1)
-b = torch.zeros_like(a)
+n_in, n_out, _ = st.arity()
+ins = [inputs.generate_torch(tuple(wl["dims"][::-1]), wl["dtype"], 1, k) for k in range(n_in)]
+outs = [torch.zeros_like(ins[0]) for _ in range(n_out)]
+pingpong = n_in == 1 and n_out == 1
 N = 400
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(N + 1)]
-for _ in range(5): st.step([a], [b])
+for _ in range(5): st.step(ins, outs)
 torch.cuda.synchronize(); time.sleep(1.0)
 with bench.ClockSampler(0) as clk:
     ev[0].record()
     for i in range(N):
-        st.step([a], [b]) if i % 2 == 0 else st.step([b], [a])
+        if pingpong and i % 2:
+            st.step(outs, ins)
+        else:
+            st.step(ins, outs)
         ev[i + 1].record()
     torch.cuda.synchronize()
 t = [ev[i].elapsed_time(ev[i + 1]) * 1e3 for i in range(N)]
