@@ -232,9 +232,25 @@ ktricubic(const __grid_constant__ TmapPack<1> tm, const __grid_constant__ TriArg
 #pragma unroll
                     for (int pp = 0; pp < NP; ++pp) {
                         const int p = 2 * pp;
-                        T2 sa = P::mul(wx[pp][0], P::mk(w[p], w[p + 1]));
+                        // w[1..V] is the LDS.128 register quad, so the operand
+                        // pair (w[e], w[e+1]) is register-aligned for odd e:
+                        // one packed FMA there, two scalar FMAs for even e
+                        // (instead of two moves to build a pair)
+                        T2 sa;
 #pragma unroll
-                        for (int a = 1; a < 4; ++a) sa = P::fma(wx[pp][a], P::mk(w[p + a], w[p + a + 1]), sa);
+                        for (int a = 0; a < 4; ++a) {
+                            const int e = p + a;
+                            if (e & 1) {
+                                sa = a == 0 ? P::mul(wx[pp][0], P::mk(w[e], w[e + 1]))
+                                            : P::fma(wx[pp][a], P::mk(w[e], w[e + 1]), sa);
+                            } else if (a == 0) {
+                                sa.x = wx[pp][0].x * w[e];
+                                sa.y = wx[pp][0].y * w[e + 1];
+                            } else {
+                                sa.x = ::fma(wx[pp][a].x, w[e], sa.x);
+                                sa.y = ::fma(wx[pp][a].y, w[e + 1], sa.y);
+                            }
+                        }
                         sb[pp] = b == 0 ? P::mul(wy[pp][0], sa) : P::fma(wy[pp][b], sa, sb[pp]);
                     }
                 }
