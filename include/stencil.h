@@ -114,6 +114,19 @@ int stencil_create(stencil_t* h, int kind, int ndims, const int64_t* dims, int d
 int stencil_set_variant(stencil_t h, int variant);
 int stencil_get_variant(stencil_t h, int* variant);
 
+/* Temporal blocking of 2-D ping-pong runs: stencil_run may
+ * apply several sweeps per kernel launch, each CTA sweeping its tile plus an
+ * S*R halo in shared memory; results are bit-identical to single sweeps.
+ *   0 (default) auto: fused for L2-resident grids (<= 8 MiB per buffer),
+ *                     where per-launch latency bounds the run
+ *   1           never fuse
+ *   S >= 2      at most S sweeps per launch (capped by shared memory)
+ * Only the register-cache variants (SHUFFLE/PLAIN) and single-GPU handles
+ * fuse; stencil_step is always one sweep.  A fused run writes the result to
+ * bufs[passes % 2] (reported in *result_idx as always) and the other buffer
+ * holds an earlier sweep. */
+int stencil_set_fusion(stencil_t h, int sweeps_per_launch);
+
 /* Arity: inputs and outputs of one step; buffers stencil_run expects
  * (2 for ping-pong kinds, 3 for wave13pt, n_in+n_out for the others). */
 int stencil_arity(stencil_t h, int* n_in, int* n_out, int* n_bufs_for_run);

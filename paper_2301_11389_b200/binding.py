@@ -24,7 +24,7 @@ STATUS = {0: "ST_OK", -1: "ST_EARG", -2: "ST_EUNSUPPORTED", -3: "ST_EALIGN",
           -4: "ST_ECUDA", -5: "ST_ENCCL", -6: "ST_ESTATE"}
 
 # Every symbol include/stencil.h declares (checked by tests/test_abi.py).
-EXPORTS = ["stencil_create", "stencil_set_variant", "stencil_get_variant", "stencil_arity",
+EXPORTS = ["stencil_create", "stencil_set_variant", "stencil_get_variant", "stencil_set_fusion", "stencil_arity",
            "stencil_info", "stencil_step", "stencil_step_range", "stencil_run", "stencil_run_host",
            "stencil_destroy", "stencil_last_error", "stencil_version", "stencil_slab_plan",
            "stencil_dist_get_id", "stencil_dist_attach"]
@@ -61,6 +61,7 @@ def lib():
                                      ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_int]
         L.stencil_set_variant.argtypes = [vp, ctypes.c_int]
         L.stencil_get_variant.argtypes = [vp, ip]
+        L.stencil_set_fusion.argtypes = [vp, ctypes.c_int]
         L.stencil_arity.argtypes = [vp, ip, ip, ip]
         L.stencil_info.argtypes = [vp, ctypes.POINTER(stencil_info_t)]
         L.stencil_step.argtypes = [vp, vpp, vpp, vp]
@@ -151,6 +152,10 @@ class Stencil:
     def set_variant(self, variant: str):
         _check(lib().stencil_set_variant(self._h, VARIANTS[variant]), "stencil_set_variant")
         self.variant = variant
+
+    def set_fusion(self, sweeps_per_launch: int):
+        """0 auto (fuse L2-resident 2-D runs), 1 off, S >= 2 sweeps per launch."""
+        _check(lib().stencil_set_fusion(self._h, int(sweeps_per_launch)), "stencil_set_fusion")
 
     def arity(self):
         a, b, c = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()

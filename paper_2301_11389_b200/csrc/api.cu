@@ -134,6 +134,16 @@ extern "C" int stencil_set_variant(stencil_t h, int variant) {
     return ST_OK;
 }
 
+extern "C" int stencil_set_fusion(stencil_t h, int sweeps_per_launch) {
+    if (!h) return set_error(ST_EARG, "null handle");
+    if (sweeps_per_launch < 0 || sweeps_per_launch > 64) return set_error(ST_EARG, "bad fusion depth");
+    h->fusion = sweeps_per_launch;
+    for (auto& g : h->graphs)          // cached graphs encode the old schedule
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    h->graphs.clear();
+    return ST_OK;
+}
+
 extern "C" int stencil_get_variant(stencil_t h, int* variant) {
     if (!h || !variant) return set_error(ST_EARG, "null argument");
     *variant = h->variant;
@@ -300,10 +310,39 @@ int stb200::ring_copy(const stencil_s* h, const void* src, void* dst, cudaStream
 // ------------------------------------------------------------------ run
 // Enqueue the whole run (ring copy + n sweeps) on stream s.  Used both for
 // graph capture and (multi-GPU) direct enqueue.
+// Sweeps per launch of a 2-D ping-pong run: the handle's fusion setting, or
+// (auto) fused when the grid is L2-resident (<= 8 MiB per buffer) and the
+// run has several sweeps: there per-launch latency, not HBM, bounds it.
+static int fusion_depth(const stencil_s* h, int n_iters) {
+    if (h->ndims != 2 || h->dist || h->k->iterable != 1 || n_iters < 2 || h->variant > ST_PLAIN) return 1;
+    const int smax = fused_max_sweeps(h);
+    if (h->fusion >= 2) return h->fusion < smax ? h->fusion : smax;
+    if (h->fusion == 1) return 1;
+    const size_t bytes = (size_t)h->ldims[0] * h->ldims[1] * (h->dtype == ST_F64 ? 8 : 4);
+    return bytes <= ((size_t)8 << 20) ? smax : 1;
+}
+
 static int enqueue_run(stencil_s* h, void* const* bufs, int n_iters, cudaStream_t s, int* result) {
     const KindInfo* k = h->k;
     int rc;
     if (k->iterable == 1) {
+        const int S = fusion_depth(h, n_iters);
+        if (S > 1) {
+            // passes of <= S sweeps (the fused kernel also writes the ring
+            // cells, so no ring copy); the result is in bufs[passes % 2]
+            const int passes = (n_iters + S - 1) / S;
+            int cur = 0, done = 0;
+            for (int p = 0; p < passes; ++p) {
+                const int sw = (n_iters - done) / (passes - p);     // even split, each >= 1
+                cudaError_t e = dispatch_2d_fused(h, bufs[cur], bufs[1 - cur], s, sw);
+                if (e != cudaSuccess)
+                    return set_error(ST_ECUDA, "%s fused launch failed: %s", k->name, cudaGetErrorString(e));
+                done += sw;
+                cur = 1 - cur;
+            }
+            *result = cur;
+            return ST_OK;
+        }
         if ((rc = ring_copy(h, bufs[0], bufs[1], s))) return rc;
         int cur = 0;
         for (int it = 0; it < n_iters; ++it) {

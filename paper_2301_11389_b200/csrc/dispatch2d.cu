@@ -4,6 +4,7 @@
 #include "internal.h"
 #include "k2d.cuh"
 #include "kpaper.cuh"
+#include "ktb2d.cuh"
 
 namespace stb200 {
 
@@ -118,6 +119,56 @@ cudaError_t dispatch_2d(stencil_s* h, const void* const* in, void* const* out, c
     case ST_GAMEOFLIFE:
         if (h->variant == ST_PLAIN) return launch_k2d<OpLife, int, VAR_PLAIN>(h, in[0], out[0], s, a, b);
         return launch_k2d<OpLife, int, VAR_SHUFFLE>(h, in[0], out[0], s, a, b);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace stb200
+
+namespace stb200 {
+
+// Temporally blocked launch: S sweeps in one kernel (ktb2d.cuh).
+template <class Op, typename T>
+static cudaError_t launch_tb(const stencil_s* h, const void* in, void* out, cudaStream_t s, int S) {
+    constexpr int R = Op::R;
+    const int64_t nx = h->ldims[0], ny = h->ldims[1];
+    const int hh = S * R;
+    const size_t smem = 2 * (size_t)(kTbTileX + 2 * hh) * (kTbTileY + 2 * hh) * sizeof(T);
+    static size_t attr = 0;
+    if (smem > attr) {
+        cudaFuncSetAttribute(ktb2d<Op, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+    }
+    const dim3 grid((unsigned)((nx - 2 * R + kTbTileX - 1) / kTbTileX),
+                    (unsigned)((ny - 2 * R + kTbTileY - 1) / kTbTileY));
+    Coeffs<T, Op::NC> c{};
+    for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)h->coeffs[t];
+    ktb2d<Op, T><<<grid, kTbThreads, smem, s>>>((const T*)in, (T*)out, nx, ny, S, c);
+    return cudaGetLastError();
+}
+
+// Largest fusion depth whose two shared-memory planes fit in ~100 KB.
+int fused_max_sweeps(const stencil_s* h) {
+    const int R = h->k->lo;
+    const size_t es = h->dtype == ST_F64 ? 8 : 4;
+    int S = 16;
+    while (S > 1 && 2 * (size_t)(kTbTileX + 2 * S * R) * (kTbTileY + 2 * S * R) * es > 100 * 1024) --S;
+    return S;
+}
+
+cudaError_t dispatch_2d_fused(stencil_s* h, const void* in, void* out, cudaStream_t s, int S) {
+    const bool f64 = h->dtype == ST_F64;
+    switch (h->k->kind) {
+    case ST_JACOBI2D5:
+        return f64 ? launch_tb<OpJacobi2D5<double>, double>(h, in, out, s, S)
+                   : launch_tb<OpJacobi2D5<float>, float>(h, in, out, s, S);
+    case ST_JACOBI2D9:
+        return f64 ? launch_tb<OpJacobi2D9<double>, double>(h, in, out, s, S)
+                   : launch_tb<OpJacobi2D9<float>, float>(h, in, out, s, S);
+    case ST_GAUSSBLUR5X5:
+        return f64 ? launch_tb<OpGauss5<double>, double>(h, in, out, s, S)
+                   : launch_tb<OpGauss5<float>, float>(h, in, out, s, S);
+    case ST_GAMEOFLIFE: return launch_tb<OpLife, int>(h, in, out, s, S);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -32,6 +32,7 @@ struct DistState;          // dist.cu
 struct stencil_s {
     const stb200::KindInfo* k = nullptr;
     int dtype = 0, ndims = 0, variant = 0, device = 0;
+    int fusion = 0;                  // 0 auto, 1 off, >= 2 sweeps per launch (2-D run)
     int64_t dims[3] = {1, 1, 1};     // global
     int64_t ldims[3] = {1, 1, 1};    // local buffers (slab + halo when attached)
     double coeffs[32] = {0};
@@ -55,6 +56,9 @@ cudaError_t dispatch_kernel(stencil_s* h, const void* const* in, void* const* ou
                             int64_t s_begin, int64_t s_end);
 int launch_sweep(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
                  int64_t s_begin, int64_t s_end);
+// dispatch2d.cu: temporally blocked 2-D sweeps
+cudaError_t dispatch_2d_fused(stencil_s* h, const void* in, void* out, cudaStream_t s, int S);
+int fused_max_sweeps(const stencil_s* h);
 int ring_copy(const stencil_s* h, const void* src, void* dst, cudaStream_t s);
 
 // dist.cu

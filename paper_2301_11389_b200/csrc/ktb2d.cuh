@@ -1,0 +1,89 @@
+// ktb2d.cuh — temporally blocked 2-D sweeps ("multiple
+// sweeps per HBM pass for tiny grids"): one launch applies S sweeps.
+//
+// For grids that sit in L2 (BASELINE configs[0], jacobi 512^2 x 10) a sweep
+// is ~1 us of work and the run is bound by per-launch latency.  Each CTA
+// loads its output tile plus a halo of S*R cells (clipped to the grid) into
+// shared memory once, applies S sweeps there (the valid region shrinks by R
+// per sweep; cells on the global boundary ring are held fixed, the Dirichlet
+// rule), and writes the tile back (edge tiles also write the ring cells).  Every cell goes through exactly the same
+// arithmetic as in a single sweep (Op::point of k2d.cuh), so the result is
+// bit-identical to S separate sweeps; the halo cells are recomputed by the
+// neighbouring tiles (redundant compute, no extra global traffic).
+#pragma once
+#include "common.cuh"
+#include "k2d.cuh"
+
+namespace stb200 {
+
+constexpr int kTbThreads = 256;                  // 32 x 8
+constexpr int kTbTileX = 64, kTbTileY = 16;     // output tile per CTA
+
+// Accessor over a shared-memory plane centred on (ly, lx): w(dj, e) is the
+// element at row ly+dj, column lx + e - R (the k2d window convention with p=0).
+template <typename T, int R>
+struct SmemWin {
+    const T* a;
+    int pitch, ly, lx;
+    __device__ __forceinline__ T operator()(int dj, int e) const { return a[(ly + dj) * pitch + lx + e - R]; }
+};
+
+// Grid: (ceil(nx_int / kTbTileX), ceil(ny_int / kTbTileY)), block 32 x 8;
+// dynamic smem = 2 * (kTbTileX + 2*S*R) * (kTbTileY + 2*S*R) * sizeof(T).
+template <class Op, typename T>
+__global__ void __launch_bounds__(kTbThreads)
+ktb2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int64_t ny, int S, Coeffs<T, Op::NC> c) {
+    constexpr int R = Op::R;
+    extern __shared__ __align__(16) unsigned char smem_tb[];
+    const int h = S * R;
+    const int pw = kTbTileX + 2 * h, ph = kTbTileY + 2 * h;
+    T* A = reinterpret_cast<T*>(smem_tb);
+    T* B = A + pw * ph;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8 threads
+    // region origin in global coordinates (may start outside the grid)
+    const int64_t gx0 = R + (int64_t)blockIdx.x * kTbTileX - h;
+    const int64_t gy0 = R + (int64_t)blockIdx.y * kTbTileY - h;
+    for (int ly = ty; ly < ph; ly += 8) {
+        const int64_t gy = gy0 + ly;
+        for (int lx = tx; lx < pw; lx += 32) {
+            const int64_t gx = gx0 + lx;
+            const T v = (gx >= 0 && gx < nx && gy >= 0 && gy < ny) ? in[gy * nx + gx] : T(0);
+            A[ly * pw + lx] = v;
+            B[ly * pw + lx] = v;                           // boundary cells keep their value
+        }
+    }
+    __syncthreads();
+    // interior of the global grid in local coordinates
+    const int ix0 = (int)(R - gx0 > 0 ? R - gx0 : 0), iy0 = (int)(R - gy0 > 0 ? R - gy0 : 0);
+    const int ix1 = (int)(nx - R - gx0 < pw ? nx - R - gx0 : pw), iy1 = (int)(ny - R - gy0 < ph ? ny - R - gy0 : ph);
+    for (int s = 1; s <= S; ++s) {
+        const int m = s * R;                               // valid after sweep s: [m, pw-m)
+        const int x0 = m > ix0 ? m : ix0, x1 = pw - m < ix1 ? pw - m : ix1;
+        const int y0 = m > iy0 ? m : iy0, y1 = ph - m < iy1 ? ph - m : iy1;
+        for (int ly = y0 + ty; ly < y1; ly += 8)
+            for (int lx = x0 + tx; lx < x1; lx += 32) {
+                const SmemWin<T, R> w{A, pw, ly, lx};
+                B[ly * pw + lx] = Op::point(w, 0, c);
+            }
+        __syncthreads();
+        T* tmp = A; A = B; B = tmp;
+    }
+    // write the tile's interior points, and the Dirichlet ring cells next to
+    // the tile when it touches the grid edge (they are unchanged from `in`, so
+    // a fused run needs no separate ring copy)
+    const bool left = blockIdx.x == 0, right = blockIdx.x == gridDim.x - 1;
+    const bool top = blockIdx.y == 0, bottom = blockIdx.y == gridDim.y - 1;
+    const int ux0 = left ? -R : 0, uy0 = top ? -R : 0;
+    const int ux1 = right ? (int)(nx - R - ((int64_t)blockIdx.x * kTbTileX + R)) + R : kTbTileX;
+    const int uy1 = bottom ? (int)(ny - R - ((int64_t)blockIdx.y * kTbTileY + R)) + R : kTbTileY;
+    for (int t = uy0 + ty; t < uy1; t += 8) {
+        const int64_t gy = R + (int64_t)blockIdx.y * kTbTileY + t;
+        if (gy >= ny) break;
+        for (int u = ux0 + tx; u < ux1; u += 32) {
+            const int64_t gx = R + (int64_t)blockIdx.x * kTbTileX + u;
+            if (gx < nx) out[gy * nx + gx] = A[(t + h) * pw + u + h];
+        }
+    }
+}
+
+}  // namespace stb200
