@@ -143,7 +143,7 @@ static cudaError_t launch_tb(const stencil_s* h, const void* in, void* out, cuda
                     (unsigned)((ny - 2 * R + kTbTileY - 1) / kTbTileY));
     Coeffs<T, Op::NC> c{};
     for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)h->coeffs[t];
-    ktb2d<Op, T><<<grid, kTbThreads, smem, s>>>((const T*)in, (T*)out, nx, ny, S, c);
+    ktb2d<Op, T><<<grid, kTbThreads, smem, s>>>((const T*)in, (T*)out, (int)nx, (int)ny, S, c);
     return cudaGetLastError();
 }
 

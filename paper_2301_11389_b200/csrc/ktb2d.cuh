@@ -30,9 +30,10 @@ struct SmemWin {
 
 // Grid: (ceil(nx_int / kTbTileX), ceil(ny_int / kTbTileY)), block 32 x 8;
 // dynamic smem = 2 * (kTbTileX + 2*S*R) * (kTbTileY + 2*S*R) * sizeof(T).
+// Only used for L2-resident grids (< 2^31 elements): 32-bit indexing.
 template <class Op, typename T>
 __global__ void __launch_bounds__(kTbThreads)
-ktb2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int64_t ny, int S, Coeffs<T, Op::NC> c) {
+ktb2d(const T* __restrict__ in, T* __restrict__ out, int nx, int ny, int S, Coeffs<T, Op::NC> c) {
     constexpr int R = Op::R;
     extern __shared__ __align__(16) unsigned char smem_tb[];
     const int h = S * R;
@@ -41,30 +42,34 @@ ktb2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int64_t ny, int
     T* B = A + pw * ph;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8 threads
     // region origin in global coordinates (may start outside the grid)
-    const int64_t gx0 = R + (int64_t)blockIdx.x * kTbTileX - h;
-    const int64_t gy0 = R + (int64_t)blockIdx.y * kTbTileY - h;
+    const int gx0 = R + (int)blockIdx.x * kTbTileX - h;
+    const int gy0 = R + (int)blockIdx.y * kTbTileY - h;
     for (int ly = ty; ly < ph; ly += 8) {
-        const int64_t gy = gy0 + ly;
+        const int gy = gy0 + ly;
+        const bool yok = gy >= 0 && gy < ny;
+        const T* src = in + (size_t)(yok ? gy : 0) * nx;
         for (int lx = tx; lx < pw; lx += 32) {
-            const int64_t gx = gx0 + lx;
-            const T v = (gx >= 0 && gx < nx && gy >= 0 && gy < ny) ? in[gy * nx + gx] : T(0);
+            const int gx = gx0 + lx;
+            const T v = (yok && gx >= 0 && gx < nx) ? src[gx] : T(0);
             A[ly * pw + lx] = v;
             B[ly * pw + lx] = v;                           // boundary cells keep their value
         }
     }
     __syncthreads();
     // interior of the global grid in local coordinates
-    const int ix0 = (int)(R - gx0 > 0 ? R - gx0 : 0), iy0 = (int)(R - gy0 > 0 ? R - gy0 : 0);
-    const int ix1 = (int)(nx - R - gx0 < pw ? nx - R - gx0 : pw), iy1 = (int)(ny - R - gy0 < ph ? ny - R - gy0 : ph);
+    const int ix0 = max(R - gx0, 0), iy0 = max(R - gy0, 0);
+    const int ix1 = min(nx - R - gx0, pw), iy1 = min(ny - R - gy0, ph);
     for (int s = 1; s <= S; ++s) {
         const int m = s * R;                               // valid after sweep s: [m, pw-m)
-        const int x0 = m > ix0 ? m : ix0, x1 = pw - m < ix1 ? pw - m : ix1;
-        const int y0 = m > iy0 ? m : iy0, y1 = ph - m < iy1 ? ph - m : iy1;
-        for (int ly = y0 + ty; ly < y1; ly += 8)
+        const int x0 = max(m, ix0), x1 = min(pw - m, ix1);
+        const int y0 = max(m, iy0), y1 = min(ph - m, iy1);
+        for (int ly = y0 + ty; ly < y1; ly += 8) {
+            T* brow = B + ly * pw;
             for (int lx = x0 + tx; lx < x1; lx += 32) {
                 const SmemWin<T, R> w{A, pw, ly, lx};
-                B[ly * pw + lx] = Op::point(w, 0, c);
+                brow[lx] = Op::point(w, 0, c);
             }
+        }
         __syncthreads();
         T* tmp = A; A = B; B = tmp;
     }
@@ -73,16 +78,13 @@ ktb2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int64_t ny, int
     // a fused run needs no separate ring copy)
     const bool left = blockIdx.x == 0, right = blockIdx.x == gridDim.x - 1;
     const bool top = blockIdx.y == 0, bottom = blockIdx.y == gridDim.y - 1;
+    const int tbx = (int)blockIdx.x * kTbTileX + R, tby = (int)blockIdx.y * kTbTileY + R;
     const int ux0 = left ? -R : 0, uy0 = top ? -R : 0;
-    const int ux1 = right ? (int)(nx - R - ((int64_t)blockIdx.x * kTbTileX + R)) + R : kTbTileX;
-    const int uy1 = bottom ? (int)(ny - R - ((int64_t)blockIdx.y * kTbTileY + R)) + R : kTbTileY;
+    const int ux1 = right ? nx - tbx : kTbTileX, uy1 = bottom ? ny - tby : kTbTileY;
     for (int t = uy0 + ty; t < uy1; t += 8) {
-        const int64_t gy = R + (int64_t)blockIdx.y * kTbTileY + t;
-        if (gy >= ny) break;
-        for (int u = ux0 + tx; u < ux1; u += 32) {
-            const int64_t gx = R + (int64_t)blockIdx.x * kTbTileX + u;
-            if (gx < nx) out[gy * nx + gx] = A[(t + h) * pw + u + h];
-        }
+        T* dst = out + (size_t)(tby + t) * nx + tbx;
+        const T* srow = A + (t + h) * pw + h;
+        for (int u = ux0 + tx; u < ux1; u += 32) dst[u] = srow[u];
     }
 }
 
