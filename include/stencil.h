@@ -36,6 +36,7 @@
 #ifndef STENCIL_B200_H
 #define STENCIL_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -210,6 +211,18 @@ int stencil_dist_get_id(uint8_t id[128]);
  * current device; afterwards local buffers have local_dims (see
  * stencil_info) and stencil_step/stencil_run exchange halos internally. */
 int stencil_dist_attach(stencil_t h, const uint8_t id[128], int rank, int nranks);
+
+/* Host transport for the halo exchange, instead of NCCL (tests, or
+ * deployments that move the planes with MPI / another library): the library
+ * copies the planes to pinned host memory and calls, for each neighbour,
+ *   fn(peer, send, send_bytes, recv, recv_bytes, user)
+ * which must send `send` to rank `peer` and receive `recv_bytes` from it
+ * into `recv` (host pointers; return 0 on success).  Synchronous: no
+ * overlap with the interior.  Same slab layout and results as
+ * stencil_dist_attach. */
+typedef int (*stencil_exchange_fn)(int peer, const void* send, size_t send_bytes, void* recv,
+                                   size_t recv_bytes, void* user);
+int stencil_dist_attach_host(stencil_t h, int rank, int nranks, stencil_exchange_fn fn, void* user);
 
 #ifdef __cplusplus
 }

@@ -27,7 +27,11 @@ STATUS = {0: "ST_OK", -1: "ST_EARG", -2: "ST_EUNSUPPORTED", -3: "ST_EALIGN",
 EXPORTS = ["stencil_create", "stencil_set_variant", "stencil_get_variant", "stencil_set_fusion", "stencil_arity",
            "stencil_info", "stencil_step", "stencil_step_range", "stencil_run", "stencil_run_host",
            "stencil_destroy", "stencil_last_error", "stencil_version", "stencil_slab_plan",
-           "stencil_dist_get_id", "stencil_dist_attach"]
+           "stencil_dist_get_id", "stencil_dist_attach", "stencil_dist_attach_host"]
+
+# int fn(int peer, const void* send, size_t send_bytes, void* recv, size_t recv_bytes, void* user)
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
+                               ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
 
 
 class StencilError(RuntimeError):
@@ -75,6 +79,7 @@ def lib():
                                         ctypes.c_int, i64p]
         L.stencil_dist_get_id.argtypes = [ctypes.c_char_p]
         L.stencil_dist_attach.argtypes = [vp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int]
+        L.stencil_dist_attach_host.argtypes = [vp, ctypes.c_int, ctypes.c_int, EXCHANGE_FN, vp]
         _lib = L
     return _lib
 
@@ -196,3 +201,25 @@ class Stencil:
 
     def attach(self, uid: bytes, rank: int, nranks: int):
         _check(lib().stencil_dist_attach(self._h, uid, rank, nranks), "stencil_dist_attach")
+
+    def attach_host(self, rank: int, nranks: int, exchange):
+        """Host-transport slab decomposition; exchange(peer, send, recv) gets
+        two uint8 numpy arrays (recv to be filled) and moves the planes, e.g.
+        with torch.distributed over gloo."""
+        import numpy as np
+
+        def _fn(peer, send, send_bytes, recv, recv_bytes, user):
+            try:
+                s_arr = np.empty(send_bytes, np.uint8)
+                ctypes.memmove(s_arr.ctypes.data, send, send_bytes)
+                r_arr = np.empty(recv_bytes, np.uint8)
+                exchange(peer, s_arr, r_arr)
+                ctypes.memmove(recv, r_arr.ctypes.data, recv_bytes)
+                return 0
+            except Exception:
+                import traceback
+                traceback.print_exc()
+                return 1
+        self._exchange_cb = EXCHANGE_FN(_fn)     # keep alive as long as the handle
+        _check(lib().stencil_dist_attach_host(self._h, rank, nranks, self._exchange_cb, None),
+               "stencil_dist_attach_host")

@@ -67,6 +67,10 @@ static NcclApi& nccl() {
 }
 
 struct DistState {
+    // transport: NCCL (default) or a host callback (stencil_dist_attach_host)
+    stencil_exchange_fn host_fn = nullptr;
+    void* host_user = nullptr;
+    char* host_buf = nullptr;        // pinned staging: send lo | send hi | recv lo | recv hi
     ncclComm_t comm = nullptr;
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t e_in = nullptr, e_comm = nullptr;
@@ -123,8 +127,55 @@ static int nccl_check(ncclResult_t r, const char* what) {
     return set_error(ST_ENCCL, "%s: %s", what, nccl().GetErrorString(r));
 }
 
+// Host transport (test / no-NCCL deployments): synchronous, no overlap.
+static int host_exchange(stencil_s* h, const void* const* in, cudaStream_t s) {
+    DistState* d = h->dist;
+    const size_t pb = d->plane_bytes;
+    const int64_t recv_lo_at = d->plan[3], send_lo_from = d->plan[4];
+    const int64_t recv_hi_at = d->plan[5], send_hi_from = d->plan[6];
+    const size_t n_lo = (size_t)(d->plan[7] & 0xFFFF), n_hi = (size_t)(d->plan[7] >> 16);
+    const unsigned mask = halo_inputs(h->k->kind);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return set_error(ST_ECUDA, "sync: %s", cudaGetErrorString(e));
+    for (int a = 0; a < h->k->n_in; ++a) {
+        if (!(mask >> a & 1u)) continue;
+        char* buf = (char*)in[a];
+        if (h->rank > 0) {
+            // staging layout: send-lo [0, n_hi) | send-hi [n_hi, n_hi+n_lo) |
+            // recv-lo [n_hi+n_lo, n_hi+2n_lo) | recv-hi [n_hi+2n_lo, 2n_hi+2n_lo) planes
+            char* snd = d->host_buf;
+            char* rcv = d->host_buf + (n_hi + n_lo) * pb;
+            cudaMemcpy(snd, buf + (size_t)send_lo_from * pb, n_hi * pb, cudaMemcpyDeviceToHost);
+            if (d->host_fn(h->rank - 1, snd, n_hi * pb, rcv, n_lo * pb, d->host_user))
+                return set_error(ST_ENCCL, "host exchange with rank %d failed", h->rank - 1);
+            cudaMemcpy(buf + (size_t)recv_lo_at * pb, rcv, n_lo * pb, cudaMemcpyHostToDevice);
+        }
+        if (h->rank < h->nranks - 1) {
+            char* snd = d->host_buf + n_hi * pb;
+            char* rcv = d->host_buf + (n_hi + 2 * n_lo) * pb;
+            cudaMemcpy(snd, buf + (size_t)send_hi_from * pb, n_lo * pb, cudaMemcpyDeviceToHost);
+            if (d->host_fn(h->rank + 1, snd, n_lo * pb, rcv, n_hi * pb, d->host_user))
+                return set_error(ST_ENCCL, "host exchange with rank %d failed", h->rank + 1);
+            cudaMemcpy(buf + (size_t)recv_hi_at * pb, rcv, n_hi * pb, cudaMemcpyHostToDevice);
+        }
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(ST_ECUDA, "host exchange copy: %s", cudaGetErrorString(e));
+    return ST_OK;
+}
+
 int dist_step(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s) {
     DistState* d = h->dist;
+    int rc;
+    int64_t a, x0, x1, b;
+    output_slabs(h, &a, &x0, &x1, &b);
+    if (d->host_fn) {                  // host transport: exchange, then all slabs
+        if ((rc = host_exchange(h, in, s))) return rc;
+        if (x0 > a && (rc = launch_sweep(h, in, out, s, a, x0))) return rc;
+        if (x1 > x0 && (rc = launch_sweep(h, in, out, s, x0, x1))) return rc;
+        if (b > x1 && (rc = launch_sweep(h, in, out, s, x1, b))) return rc;
+        return ST_OK;
+    }
     NcclApi& api = nccl();
     const size_t pb = d->plane_bytes;
     const bool has_lower = h->rank > 0, has_upper = h->rank < h->nranks - 1;
@@ -134,16 +185,15 @@ int dist_step(stencil_s* h, const void* const* in, void* const* out, cudaStream_
     if ((e = cudaEventRecord(d->e_in, s)) != cudaSuccess ||
         (e = cudaStreamWaitEvent(d->comm_stream, d->e_in, 0)) != cudaSuccess)
         return set_error(ST_ECUDA, "event: %s", cudaGetErrorString(e));
-    int rc;
     if ((rc = nccl_check(api.GroupStart(), "ncclGroupStart"))) return rc;
     const unsigned mask = halo_inputs(h->k->kind);
     // offsets and counts straight from the host plan (stencil_slab_plan)
     const int64_t recv_lo_at = d->plan[3], send_lo_from = d->plan[4];
     const int64_t recv_hi_at = d->plan[5], send_hi_from = d->plan[6];
     const size_t n_lo = (size_t)(d->plan[7] & 0xFFFF), n_hi = (size_t)(d->plan[7] >> 16);
-    for (int a = 0; a < h->k->n_in; ++a) {
-        if (!(mask >> a & 1u)) continue;
-        char* buf = (char*)in[a];      // the halo planes of an input are the exchange's
+    for (int ai = 0; ai < h->k->n_in; ++ai) {
+        if (!(mask >> ai & 1u)) continue;
+        char* buf = (char*)in[ai];     // the halo planes of an input are the exchange's
         if (has_lower) {               // my bottom hi owned planes <-> rank-1's top lo planes
             api.Send(buf + (size_t)send_lo_from * pb, n_hi * pb, kNcclInt8, h->rank - 1, d->comm, d->comm_stream);
             api.Recv(buf + (size_t)recv_lo_at * pb, n_lo * pb, kNcclInt8, h->rank - 1, d->comm, d->comm_stream);
@@ -159,8 +209,6 @@ int dist_step(stencil_s* h, const void* const* in, void* const* out, cudaStream_
         return set_error(ST_ECUDA, "event: %s", cudaGetErrorString(e));
 
     // 2. interior planes (overlap the exchange), 3. halo-dependent slabs
-    int64_t a, x0, x1, b;
-    output_slabs(h, &a, &x0, &x1, &b);
     if (x1 > x0 && (rc = launch_sweep(h, in, out, s, x0, x1))) return rc;
     if ((e = cudaStreamWaitEvent(s, d->e_comm, 0)) != cudaSuccess)
         return set_error(ST_ECUDA, "event wait: %s", cudaGetErrorString(e));
@@ -173,6 +221,7 @@ void dist_release(stencil_s* h) {
     DistState* d = h->dist;
     if (!d) return;
     if (d->comm && nccl().ok) nccl().CommDestroy(d->comm);
+    if (d->host_buf) cudaFreeHost(d->host_buf);
     if (d->e_in) cudaEventDestroy(d->e_in);
     if (d->e_comm) cudaEventDestroy(d->e_comm);
     if (d->comm_stream) cudaStreamDestroy(d->comm_stream);
@@ -221,16 +270,15 @@ extern "C" int stencil_dist_get_id(uint8_t id[128]) {
     return ST_OK;
 }
 
-extern "C" int stencil_dist_attach(stencil_t h, const uint8_t id[128], int rank, int nranks) {
-    if (!h || !id) return set_error(ST_EARG, "null argument");
+// Common part of attaching: plan, streams/events, local dims.
+static int attach_common(stencil_t h, int rank, int nranks, DistState** out) {
+    if (!h) return set_error(ST_EARG, "null handle");
     if (h->dist) return set_error(ST_ESTATE, "handle already attached");
     if (!h->graphs.empty()) return set_error(ST_ESTATE, "attach before the first run");
     const int slow = h->ndims - 1;
     int64_t plan[8];
     int rc = stencil_slab_plan(h->dims[slow], h->k->lo, h->k->hi, rank, nranks, plan);
     if (rc) return rc;
-    NcclApi& api = nccl();
-    if (!api.ok) return set_error(ST_ENCCL, "libnccl.so.2 not loadable");
     cudaSetDevice(h->device);
     DistState* d = new DistState();
     d->n = h->dims[slow];
@@ -246,6 +294,24 @@ extern "C" int stencil_dist_attach(stencil_t h, const uint8_t id[128], int rank,
         dist_release(h);
         return set_error(ST_ECUDA, "attach: %s", cudaGetErrorString(e));
     }
+    *out = d;
+    return ST_OK;
+}
+
+static void attach_finish(stencil_t h, DistState* d, int rank, int nranks) {
+    h->dist = d;
+    h->rank = rank;
+    h->nranks = nranks;
+    h->ldims[h->ndims - 1] = d->plan[2];
+}
+
+extern "C" int stencil_dist_attach(stencil_t h, const uint8_t id[128], int rank, int nranks) {
+    if (!id) return set_error(ST_EARG, "null id");
+    NcclApi& api = nccl();
+    if (!api.ok) return set_error(ST_ENCCL, "libnccl.so.2 not loadable");
+    DistState* d = nullptr;
+    int rc = attach_common(h, rank, nranks, &d);
+    if (rc) return rc;
     ncclUniqueId u;
     memcpy(u.internal, id, 128);
     rc = nccl_check(api.CommInitRank(&d->comm, nranks, u, rank), "ncclCommInitRank");
@@ -255,9 +321,25 @@ extern "C" int stencil_dist_attach(stencil_t h, const uint8_t id[128], int rank,
         dist_release(h);
         return rc;
     }
-    h->dist = d;
-    h->rank = rank;
-    h->nranks = nranks;
-    h->ldims[slow] = plan[2];
+    attach_finish(h, d, rank, nranks);
+    return ST_OK;
+}
+
+extern "C" int stencil_dist_attach_host(stencil_t h, int rank, int nranks, stencil_exchange_fn fn,
+                                        void* user) {
+    if (!fn) return set_error(ST_EARG, "null exchange function");
+    DistState* d = nullptr;
+    int rc = attach_common(h, rank, nranks, &d);
+    if (rc) return rc;
+    const size_t n_lo = (size_t)(d->plan[7] & 0xFFFF), n_hi = (size_t)(d->plan[7] >> 16);
+    cudaError_t e = cudaMallocHost(&d->host_buf, 2 * (n_lo + n_hi) * d->plane_bytes);
+    if (e != cudaSuccess) {
+        h->dist = d;
+        dist_release(h);
+        return set_error(ST_ECUDA, "pinned staging: %s", cudaGetErrorString(e));
+    }
+    d->host_fn = fn;
+    d->host_user = user;
+    attach_finish(h, d, rank, nranks);
     return ST_OK;
 }
