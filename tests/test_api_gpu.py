@@ -1,0 +1,98 @@
+"""C-ABI behaviour on the GPU: end-to-end host-buffer runs, argument errors,
+graph cache, variant switching, stream semantics."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2301_11389_b200 import inputs
+from paper_2301_11389_b200.binding import Stencil, StencilError
+from parity import assert_parity
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("kind,dtype,shape,n", [
+    ("gaussblur5x5", "f32", (130, 260), 3), ("wave13pt", "f64", (12, 14, 66), 4),
+    ("gradient", "f32", (9, 10, 132), 2), ("tricubic", "f32", (8, 19, 132), 1)])
+def test_run_host_matches_oracle(oracle, kind, dtype, shape, n):
+    ar = oracle.arity(kind)
+    ins = [inputs.generate_np(shape, dtype, inputs.BASE_SEED + 31, a) for a in range(ar["n_in"])]
+    if ar["n_bufs"] == 2:
+        bufs, n_up, n_down = [ins[0], np.zeros_like(ins[0])], 1, 1
+    elif kind == "wave13pt":
+        bufs, n_up, n_down = [ins[0], ins[1], np.zeros_like(ins[0])], 2, 1
+    else:
+        bufs = ins + [np.zeros_like(ins[0]) for _ in range(ar["n_out"])]
+        n_up, n_down = ar["n_in"], ar["n_out"]
+    ob = [b.copy() for b in bufs]
+    ridx = oracle.run(kind, dtype, ob, n)
+    st = Stencil(kind, shape[::-1], dtype)
+    dev = [torch.zeros(shape, dtype=torch.from_numpy(ins[0]).dtype, device="cuda") for _ in bufs]
+    h_in = [torch.from_numpy(b.copy()).pin_memory() for b in bufs[:n_up]]
+    h_out = [torch.empty(shape, dtype=h_in[0].dtype).pin_memory() for _ in range(n_down)]
+    st.run_host(h_in, h_out, dev, n)
+    for k in range(n_down):
+        assert_parity(h_out[k].numpy(), ob[ridx + k], dtype, f"{kind} run_host out{k}")
+
+
+def test_argument_errors():
+    st = Stencil("jacobi2d5", (64, 32), "f32")
+    a = torch.zeros((32, 64), device="cuda")
+    with pytest.raises(StencilError) as e:
+        st.step([a], [a])                                   # aliasing
+    assert e.value.code == -1
+    big = torch.zeros(32 * 64 + 1, device="cuda")
+    with pytest.raises(StencilError) as e:
+        st.step([big[1:]], [a])                             # 4-byte offset: not 16-B aligned
+    assert e.value.code == -3
+    with pytest.raises(StencilError):
+        st.run([a, a], 2)                                   # aliasing run buffers
+    with pytest.raises(StencilError):
+        st.step_range([a], [torch.zeros_like(a)], 0, 5)     # range includes the boundary row
+    with pytest.raises(StencilError):
+        st.run([a, torch.zeros_like(a)], -1)
+
+
+def test_graph_cache_and_variant_switch(oracle):
+    shape = (40, 136)
+    f = inputs.generate_np(shape, "f32", 5)
+    bufs = [f.copy(), np.zeros_like(f)]
+    ridx = oracle.run("jacobi2d9", "f32", bufs, 4)
+    st = Stencil("jacobi2d9", shape[::-1], "f32")
+    st.set_fusion(1)
+    d = [torch.from_numpy(f).cuda(), torch.zeros(shape, device="cuda")]
+    results = []
+    for var in ("shuffle", "plain", "paper_ptxasw", "shuffle"):
+        st.set_variant(var)
+        d[0].copy_(torch.from_numpy(f))
+        idx = st.run(d, 4)                                  # cached graph per (bufs, n, variant)
+        torch.cuda.synchronize()
+        results.append(d[idx].cpu().numpy().copy())
+        assert_parity(results[-1], bufs[ridx], "f32", var)
+    for r in results[1:]:
+        assert np.array_equal(r.view(np.uint8), results[0].view(np.uint8))
+
+
+def test_run_on_a_side_stream_and_zero_iterations():
+    shape = (20, 132)
+    f = inputs.generate_np(shape, "f32", 6)
+    st = Stencil("gaussblur5x5", shape[::-1], "f32")
+    a = torch.from_numpy(f).cuda()
+    b = torch.full(shape, 3.0, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        idx = st.run([a, b], 0, stream=s)                   # only the ring copy
+    s.synchronize()
+    assert idx == 0
+    ring = np.ones(shape, bool)
+    ring[2:-2, 2:-2] = False
+    bb = b.cpu().numpy()
+    assert np.array_equal(bb[ring], f[ring]) and np.all(bb[~ring] == 3.0)
+
+
+def test_info_fields():
+    st = Stencil("wave13pt", (66, 20, 16), "f64")
+    i = st.info()
+    assert i["interior_points"] == 62 * 16 * 12
+    assert i["bytes_per_point"] == 24.0 and i["launches_per_step"] == 1
+    assert i["lo"] == 2 and i["hi"] == 2 and i["nranks"] == 1
