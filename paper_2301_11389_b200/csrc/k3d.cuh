@@ -336,16 +336,10 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
 #pragma unroll
                             for (int k = 0; k < R; ++k) x.xw[a][R + V + k] = shfl_down(v[k], 1);
                             // warp edge (%out_of_range): the
-                            // fallback read of the staged neighbour sector
-                            const int e = lane0 ? -R : V;
-                            T hv[R];
-#pragma unroll
-                            for (int k = 0; k < R; ++k) hv[k] = b[off(a, r, 0, e + k)];
-#pragma unroll
-                            for (int k = 0; k < R; ++k) {
-                                x.xw[a][k] = lane0 ? hv[k] : x.xw[a][k];
-                                x.xw[a][R + V + k] = lane31 ? hv[k] : x.xw[a][R + V + k];
-                            }
+                            // fallback read of the staged neighbour sector,
+                            // predicated (no branch, no select)
+                            lds_pred<T, R>(lane0, b + off(a, r, 0, -R), &x.xw[a][0]);
+                            lds_pred<T, R>(lane31, b + off(a, r, 0, V), &x.xw[a][R + V]);
                         } else {                          // PLAIN: neighbours' elements from smem
 #pragma unroll
                             for (int k = 0; k < R; ++k) x.xw[a][k] = b[off(a, r, 0, k - R)];
