@@ -346,6 +346,31 @@ def main():
     k_ms = sorted(a.elapsed_time(b) for a, b in k_ev[1:])
     k_med = k_ms[len(k_ms) // 2]
 
+    # ---- the other variant of the paper's question (shuffle vs plain), same timing
+    other = "plain" if args.variant == "shuffle" else "shuffle"
+    variants = {args.variant: value}
+    if args.variant in ("shuffle", "plain"):
+        st.set_variant(other)
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        o_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(max(3, args.steps // 2))]
+        if world > 1:
+            dist.barrier()
+        for a, b in o_ev:
+            if flush is not None:
+                flush.fill_(1.0)
+            a.record(stream)
+            step()
+            b.record(stream)
+        torch.cuda.synchronize()
+        o_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in o_ev)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(o_ms, op=dist.ReduceOp.MAX)
+        variants[other] = pts_all * iters * len(o_ev) / (float(o_ms.item()) / 1e3) / 1e9
+        st.set_variant(args.variant)
+
     # ---- end to end through the C ABI with HOST buffers
     e2e = None
     if not args.no_e2e:
@@ -396,6 +421,7 @@ def main():
                          "kernel_only_us": k_med * 1e3,
                          "kernel_only_frac": alg_bytes / (k_med / 1e3) / 1e9 / peak},
             "clocks": clocks,
+            "variants": {k: round(v, 2) for k, v in variants.items()},
             "e2e": e2e,
             "gpu_launches": args.steps * (launches + (2 if wl["kind"] == "wave13pt" else
                                                        (1 if n_bufs == 2 else 0))),
