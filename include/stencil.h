@@ -123,9 +123,9 @@ int stencil_get_variant(stencil_t h, int* variant);
  *   1           never fuse
  *   S >= 2      at most S sweeps per launch (capped by shared memory)
  * Only the register-cache variants (SHUFFLE/PLAIN) and single-GPU handles
- * fuse; stencil_step is always one sweep.  A fused run writes the result to
- * bufs[passes % 2] (reported in *result_idx as always) and the other buffer
- * holds an earlier sweep. */
+ * fuse; stencil_step is always one sweep.  A fused run leaves the result in
+ * bufs[n_iters % 2] like single sweeps; the other buffer holds an earlier
+ * sweep. */
 int stencil_set_fusion(stencil_t h, int sweeps_per_launch);
 
 /* Arity: inputs and outputs of one step; buffers stencil_run expects
@@ -223,6 +223,24 @@ int stencil_dist_attach(stencil_t h, const uint8_t id[128], int rank, int nranks
 typedef int (*stencil_exchange_fn)(int peer, const void* send, size_t send_bytes, void* recv,
                                    size_t recv_bytes, void* user);
 int stencil_dist_attach_host(stencil_t h, int rank, int nranks, stencil_exchange_fn fn, void* user);
+
+/* Fused halo exchange over peer memory (the "compute + collective in one
+ * kernel" transport): the kernels that compute a rank's boundary planes also
+ * store them straight into the neighbours' buffers through CUDA-IPC peer
+ * pointers (NVLink / NVSwitch P2P), and ranks order themselves with epoch
+ * flags in device memory (stream memory operations, no spinning SMs).
+ *   1. stencil_dist_attach_p2p(h, rank, nranks)
+ *   2. for a set of run buffers: stencil_p2p_export writes a blob (IPC
+ *      handles of the rank's flags and buffers); all-gather the blobs (e.g.
+ *      torch.distributed); stencil_p2p_import(h, bufs, n, blob of rank-1,
+ *      blob of rank+1) maps the neighbours' buffers (NULL where none)
+ *   3. stencil_run / stencil_step with exactly those buffers.
+ * Buffers must be plain device allocations (cudaMalloc / torch default
+ * allocator).  Same slab layout and results as stencil_dist_attach. */
+int stencil_dist_attach_p2p(stencil_t h, int rank, int nranks);
+int stencil_p2p_export(stencil_t h, void* const* bufs, int nbufs, uint8_t* blob, size_t cap, size_t* len);
+int stencil_p2p_import(stencil_t h, void* const* bufs, int nbufs, const uint8_t* lower_blob,
+                       const uint8_t* upper_blob);
 
 #ifdef __cplusplus
 }

@@ -27,7 +27,8 @@ STATUS = {0: "ST_OK", -1: "ST_EARG", -2: "ST_EUNSUPPORTED", -3: "ST_EALIGN",
 EXPORTS = ["stencil_create", "stencil_set_variant", "stencil_get_variant", "stencil_set_fusion", "stencil_arity",
            "stencil_info", "stencil_step", "stencil_step_range", "stencil_run", "stencil_run_host",
            "stencil_destroy", "stencil_last_error", "stencil_version", "stencil_slab_plan",
-           "stencil_dist_get_id", "stencil_dist_attach", "stencil_dist_attach_host"]
+           "stencil_dist_get_id", "stencil_dist_attach", "stencil_dist_attach_host",
+           "stencil_dist_attach_p2p", "stencil_p2p_export", "stencil_p2p_import"]
 
 # int fn(int peer, const void* send, size_t send_bytes, void* recv, size_t recv_bytes, void* user)
 EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
@@ -80,6 +81,10 @@ def lib():
         L.stencil_dist_get_id.argtypes = [ctypes.c_char_p]
         L.stencil_dist_attach.argtypes = [vp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int]
         L.stencil_dist_attach_host.argtypes = [vp, ctypes.c_int, ctypes.c_int, EXCHANGE_FN, vp]
+        L.stencil_dist_attach_p2p.argtypes = [vp, ctypes.c_int, ctypes.c_int]
+        L.stencil_p2p_export.argtypes = [vp, vpp, ctypes.c_int, ctypes.c_char_p, ctypes.c_size_t,
+                                         ctypes.POINTER(ctypes.c_size_t)]
+        L.stencil_p2p_import.argtypes = [vp, vpp, ctypes.c_int, ctypes.c_char_p, ctypes.c_char_p]
         _lib = L
     return _lib
 
@@ -201,6 +206,26 @@ class Stencil:
 
     def attach(self, uid: bytes, rank: int, nranks: int):
         _check(lib().stencil_dist_attach(self._h, uid, rank, nranks), "stencil_dist_attach")
+
+    def attach_p2p(self, rank: int, nranks: int):
+        """Fused peer-store halo transport (see stencil.h)."""
+        _check(lib().stencil_dist_attach_p2p(self._h, rank, nranks), "stencil_dist_attach_p2p")
+        self._rank, self._nranks = rank, nranks
+
+    def p2p_register(self, bufs, allgather):
+        """Export this rank's buffers, all-gather the blobs with
+        allgather(bytes) -> list of bytes (one per rank), import the
+        neighbours'.  Call on every rank with the run's buffers."""
+        cap = 8 + 72 * (len(bufs) + 1)
+        blob = ctypes.create_string_buffer(cap)
+        n = ctypes.c_size_t()
+        _check(lib().stencil_p2p_export(self._h, _ptrs(bufs), len(bufs), blob, cap, ctypes.byref(n)),
+               "stencil_p2p_export")
+        blobs = allgather(blob.raw[: n.value])
+        r, w = self._rank, self._nranks
+        lo = blobs[r - 1] if r > 0 else None
+        hi = blobs[r + 1] if r < w - 1 else None
+        _check(lib().stencil_p2p_import(self._h, _ptrs(bufs), len(bufs), lo, hi), "stencil_p2p_import")
 
     def attach_host(self, rank: int, nranks: int, exchange):
         """Host-transport slab decomposition; exchange(peer, send, recv) gets

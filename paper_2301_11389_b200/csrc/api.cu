@@ -325,12 +325,16 @@ static int fusion_depth(const stencil_s* h, int n_iters) {
 static int enqueue_run(stencil_s* h, void* const* bufs, int n_iters, cudaStream_t s, int* result) {
     const KindInfo* k = h->k;
     int rc;
+    if (dist_is_p2p(h)) return p2p_run(h, bufs, n_iters, s, result);
     if (k->iterable == 1) {
         const int S = fusion_depth(h, n_iters);
         if (S > 1) {
             // passes of <= S sweeps (the fused kernel also writes the ring
-            // cells, so no ring copy); the result is in bufs[passes % 2]
-            const int passes = (n_iters + S - 1) / S;
+            // cells, so no ring copy), an even/odd count matching n_iters so
+            // the result lands in bufs[n_iters % 2] exactly as with single
+            // sweeps (runs chain the same way)
+            int passes = (n_iters + S - 1) / S;
+            if ((passes & 1) != (n_iters & 1)) ++passes;
             int cur = 0, done = 0;
             for (int p = 0; p < passes; ++p) {
                 const int sw = (n_iters - done) / (passes - p);     // even split, each >= 1

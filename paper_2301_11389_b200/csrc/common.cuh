@@ -93,6 +93,16 @@ __device__ __forceinline__ double shfl_down(double v, int d){ return __shfl_down
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// Fused halo exchange (dist.cu P2P transport): the output planes/rows a
+// neighbour rank needs as halo are also stored straight into its buffer
+// through a peer pointer.  Slow-axis index q < lo_end goes to `lo` at element
+// offset + d_lo; q >= hi_begin goes to `hi` at offset + d_hi.  Null = off.
+template <typename T> struct PeerOut {
+    T* lo = nullptr;
+    T* hi = nullptr;
+    int64_t lo_end = 0, hi_begin = 0, d_lo = 0, d_hi = 0;
+};
+
 // Coefficients passed by value as a kernel parameter (constant bank): FFMA
 // reads them as c[bank][offset] operands, no registers spent.
 template <typename T, int N> struct Coeffs { T c[N > 0 ? N : 1]; };

@@ -53,8 +53,15 @@ static cudaError_t launch_k2d(const stencil_s* h, const void* in, void* out, cud
     if (nstrips > 65535) return cudaErrorInvalidConfiguration;
     Coeffs<T, Op::NC> c{};
     for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)h->coeffs[t];
+    PeerOut<T> peer;
+    peer.lo = (T*)h->peer_lo;
+    peer.hi = (T*)h->peer_hi;
+    peer.lo_end = h->peer_lo_end;
+    peer.hi_begin = h->peer_hi_begin;
+    peer.d_lo = h->peer_d_lo;
+    peer.d_hi = h->peer_d_hi;
     kern<<<dim3((unsigned)gx, (unsigned)nstrips), k2d_threads(), smem, s>>>(
-        (const T*)in, (T*)out, nx, (int)y_lo, (int)y_hi, (int)H, c);
+        (const T*)in, (T*)out, nx, (int)y_lo, (int)y_hi, (int)H, c, peer);
     return cudaGetLastError();
 }
 

@@ -94,6 +94,12 @@ static cudaError_t launch_k3d(const stencil_s* h, const void* const* in, void* c
     const int64_t grid = (items + m - 1) / m;
     args.zsplit = (int)zsplit;
     args.m = (int)m;
+    args.peer.lo = (T*)h->peer_lo;
+    args.peer.hi = (T*)h->peer_hi;
+    args.peer.lo_end = h->peer_lo_end;
+    args.peer.hi_begin = h->peer_hi_begin;
+    args.peer.d_lo = h->peer_d_lo;
+    args.peer.d_hi = h->peer_d_hi;
     static const int dbg_zc = getenv("STB200_3D_ZC") ? atoi(getenv("STB200_3D_ZC")) : 0;
     // chunk depth (measured): the single-array radius-1 kinds
     // run 13-17% faster with 6-plane chunks (tighter lockstep) despite the

@@ -24,12 +24,7 @@
 #include <cstring>
 
 #include "internal.h"
-
-// Minimal NCCL ABI subset (nccl.h, NCCL 2.x; stable since 2.0).
-typedef struct ncclComm* ncclComm_t;
-typedef int ncclResult_t;                       // ncclSuccess = 0
-typedef struct { char internal[128]; } ncclUniqueId;
-static const int kNcclInt8 = 0;                 // ncclInt8 == ncclChar
+#include "dist_state.h"
 
 namespace stb200 {
 
@@ -65,19 +60,6 @@ static NcclApi& nccl() {
     }
     return api;
 }
-
-struct DistState {
-    // transport: NCCL (default) or a host callback (stencil_dist_attach_host)
-    stencil_exchange_fn host_fn = nullptr;
-    void* host_user = nullptr;
-    char* host_buf = nullptr;        // pinned staging: send lo | send hi | recv lo | recv hi
-    ncclComm_t comm = nullptr;
-    cudaStream_t comm_stream = nullptr;
-    cudaEvent_t e_in = nullptr, e_comm = nullptr;
-    int64_t n = 0, m = 0;            // global slow extent, planes per rank
-    int64_t plan[8] = {0};
-    size_t plane_bytes = 0;
-};
 
 // Inputs with taps along the slow axis (their halo planes must be exchanged).
 static unsigned halo_inputs(int kind) {
@@ -164,8 +146,16 @@ static int host_exchange(stencil_s* h, const void* const* in, cudaStream_t s) {
     return ST_OK;
 }
 
+bool dist_is_p2p(const stencil_s* h) { return h->dist && h->dist->p2p; }
+
+void dist_output_slabs(const stencil_s* h, int64_t* a, int64_t* x0, int64_t* x1, int64_t* b) {
+    output_slabs(h, a, x0, x1, b);
+}
+unsigned dist_halo_inputs(int kind) { return halo_inputs(kind); }
+
 int dist_step(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s) {
     DistState* d = h->dist;
+    if (d->p2p) return p2p_step(h, in, out, s);
     int rc;
     int64_t a, x0, x1, b;
     output_slabs(h, &a, &x0, &x1, &b);
@@ -222,6 +212,7 @@ void dist_release(stencil_s* h) {
     if (!d) return;
     if (d->comm && nccl().ok) nccl().CommDestroy(d->comm);
     if (d->host_buf) cudaFreeHost(d->host_buf);
+    if (d->p2p) p2p_release(d);
     if (d->e_in) cudaEventDestroy(d->e_in);
     if (d->e_comm) cudaEventDestroy(d->e_comm);
     if (d->comm_stream) cudaStreamDestroy(d->comm_stream);
@@ -271,7 +262,7 @@ extern "C" int stencil_dist_get_id(uint8_t id[128]) {
 }
 
 // Common part of attaching: plan, streams/events, local dims.
-static int attach_common(stencil_t h, int rank, int nranks, DistState** out) {
+int dist_attach_common(stencil_t h, int rank, int nranks, DistState** out) {
     if (!h) return set_error(ST_EARG, "null handle");
     if (h->dist) return set_error(ST_ESTATE, "handle already attached");
     if (!h->graphs.empty()) return set_error(ST_ESTATE, "attach before the first run");
@@ -298,7 +289,7 @@ static int attach_common(stencil_t h, int rank, int nranks, DistState** out) {
     return ST_OK;
 }
 
-static void attach_finish(stencil_t h, DistState* d, int rank, int nranks) {
+void dist_attach_finish(stencil_t h, DistState* d, int rank, int nranks) {
     h->dist = d;
     h->rank = rank;
     h->nranks = nranks;
@@ -310,7 +301,7 @@ extern "C" int stencil_dist_attach(stencil_t h, const uint8_t id[128], int rank,
     NcclApi& api = nccl();
     if (!api.ok) return set_error(ST_ENCCL, "libnccl.so.2 not loadable");
     DistState* d = nullptr;
-    int rc = attach_common(h, rank, nranks, &d);
+    int rc = dist_attach_common(h, rank, nranks, &d);
     if (rc) return rc;
     ncclUniqueId u;
     memcpy(u.internal, id, 128);
@@ -321,7 +312,7 @@ extern "C" int stencil_dist_attach(stencil_t h, const uint8_t id[128], int rank,
         dist_release(h);
         return rc;
     }
-    attach_finish(h, d, rank, nranks);
+    dist_attach_finish(h, d, rank, nranks);
     return ST_OK;
 }
 
@@ -329,7 +320,7 @@ extern "C" int stencil_dist_attach_host(stencil_t h, int rank, int nranks, stenc
                                         void* user) {
     if (!fn) return set_error(ST_EARG, "null exchange function");
     DistState* d = nullptr;
-    int rc = attach_common(h, rank, nranks, &d);
+    int rc = dist_attach_common(h, rank, nranks, &d);
     if (rc) return rc;
     const size_t n_lo = (size_t)(d->plan[7] & 0xFFFF), n_hi = (size_t)(d->plan[7] >> 16);
     cudaError_t e = cudaMallocHost(&d->host_buf, 2 * (n_lo + n_hi) * d->plane_bytes);
@@ -340,6 +331,6 @@ extern "C" int stencil_dist_attach_host(stencil_t h, int rank, int nranks, stenc
     }
     d->host_fn = fn;
     d->host_user = user;
-    attach_finish(h, d, rank, nranks);
+    dist_attach_finish(h, d, rank, nranks);
     return ST_OK;
 }

@@ -41,6 +41,10 @@ struct stencil_s {
     std::vector<int> tmaps;          // reserved
     // multi-GPU
     stb200::DistState* dist = nullptr;
+    // fused halo stores for the next launch (dist.cu P2P transport; null = off)
+    void* peer_lo = nullptr;
+    void* peer_hi = nullptr;
+    int64_t peer_lo_end = 0, peer_hi_begin = 0, peer_d_lo = 0, peer_d_hi = 0;
     int rank = 0, nranks = 1;
 };
 
@@ -67,5 +71,7 @@ void dist_release(stencil_s* h);
 int64_t dist_owned_interior_points(const stencil_s* h);
 int dist_launches_per_step(const stencil_s* h);
 void dist_ring_planes(const stencil_s* h, int64_t* full_lo, int64_t* full_hi);
+bool dist_is_p2p(const stencil_s* h);
+int p2p_run(stencil_s* h, void* const* bufs, int n_iters, cudaStream_t s, int* result);
 
 }  // namespace stb200

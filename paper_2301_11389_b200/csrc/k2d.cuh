@@ -155,7 +155,7 @@ constexpr int k2d_threads() { return (kWarps2D + 1) * 32; }
 template <class Op, typename T, int VARIANT>
 __global__ void __launch_bounds__(k2d_threads())
 k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_hi, int H,
-    Coeffs<T, Op::NC> c) {
+    Coeffs<T, Op::NC> c, PeerOut<T> peer) {
     constexpr int R = Op::R;
     constexpr int V = vlen<T>();
     constexpr int PAD = V;                 // 16 bytes of halo room each side
@@ -269,7 +269,8 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
     auto sweep = [&](auto edge_tag) {
         constexpr bool EDGE = decltype(edge_tag)::value;
         T* optr = out + (int64_t)ys * nx + xl;             // running output pointer
-        auto emit = [&](int u) {
+        const bool fused = peer.lo != nullptr || peer.hi != nullptr;
+        auto emit = [&](int u, int yrow) {
             T o[V];
             const Win<T, NW, W, R> w{win, u};
             if constexpr (HasPaired<Op>::value) {                       // S6
@@ -283,13 +284,20 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
 #pragma unroll
                 for (int p = 0; p < V; ++p) o[p] = Op::point(w, p, cr);
             }
-            if constexpr (!EDGE) {
-                stg_vec(optr, o);                                       // S7
-            } else {
-                if (vec_store) stg_vec(optr, o);
+            auto store = [&](T* dst) {
+                if constexpr (!EDGE) {
+                    stg_vec(dst, o);                                    // S7
+                } else {
+                    if (vec_store) stg_vec(dst, o);
 #pragma unroll
-                for (int p = 0; p < V; ++p)
-                    if (el_store[p]) optr[p] = o[p];
+                    for (int p = 0; p < V; ++p)
+                        if (el_store[p]) dst[p] = o[p];
+                }
+            };
+            store(optr);
+            if (fused) {                                   // warp-uniform: halo rows to the peers
+                if (peer.lo && yrow < peer.lo_end) store(peer.lo + (optr - out) + peer.d_lo);
+                if (peer.hi && yrow >= peer.hi_begin) store(peer.hi + (optr - out) + peer.d_hi);
             }
             optr += nx;
         };
@@ -298,14 +306,14 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
 #pragma unroll
             for (int u = 0; u < NW; ++u) {
                 consume((unsigned)(y + u - ys + 2 * R), win[(u + 2 * R) % NW]);
-                emit(u);
+                emit(u, y + u);
             }
         }
 #pragma unroll
         for (int u = 0; u < NW - 1; ++u) {                 // remainder (< NW rows)
             if (y + u < ye) {
                 consume((unsigned)(y + u - ys + 2 * R), win[(u + 2 * R) % NW]);
-                emit(u);
+                emit(u, y + u);
             }
         }
     };

@@ -217,6 +217,7 @@ struct K3Args {
     int z_lo, nzo;         // output planes [z_lo, z_lo + nzo)
     int ntx, nty;          // tile counts
     int zsplit, zc, m;     // LockIter: z parts per column, chunk planes, items per CTA
+    PeerOut<T> peer;       // fused halo stores of out[0] (P2P multi-GPU), off when null
     int dbg;               // experiment switches (0 in production)
 };
 
@@ -292,6 +293,8 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
 #pragma unroll
         for (int p = 0; p < V; ++p) x_el[p] = !x_vec && own && xl + p >= R && xl + p < args.nx - R;
         int64_t obase = ((int64_t)(args.z_lo + zo) * args.ny + y0) * args.nx + xl;
+        int64_t zcur = args.z_lo + zo;                     // output plane of the next emit
+        const bool fused = args.peer.lo != nullptr || args.peer.hi != nullptr;
         const int np = nseg + 2 * R;
 
         // element offset of (row warp*RY + r + dy, lane vector + e) in array a's box
@@ -365,17 +368,24 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
                     for (int k = 0; k < Op::NOUT; ++k) o[k][p] = res[k];
                 }
                 const bool row_ok = y0 + r >= R && y0 + r < args.ny - R;
-#pragma unroll
-                for (int k = 0; k < Op::NOUT; ++k) {
-                    T* op = args.out[k] + obase + r * args.nx;
-                    if (row_ok && x_vec) stg_vec(op, o[k]);
+                auto store = [&](T* op, const T* ov) {
+                    if (row_ok && x_vec) stg_vec(op, ov);
 #pragma unroll
                     for (int p = 0; p < V; ++p)
-                        if (row_ok && x_el[p]) op[p] = o[k][p];
+                        if (row_ok && x_el[p]) op[p] = ov[p];
+                };
+#pragma unroll
+                for (int k = 0; k < Op::NOUT; ++k) store(args.out[k] + obase + r * args.nx, o[k]);
+                if (fused) {                               // halo planes straight to the peers
+                    if (args.peer.lo && zcur < args.peer.lo_end)
+                        store(args.peer.lo + obase + r * args.nx + args.peer.d_lo, o[0]);
+                    if (args.peer.hi && zcur >= args.peer.hi_begin)
+                        store(args.peer.hi + obase + r * args.nx + args.peer.d_hi, o[0]);
                 }
             }
             release(gg);
             obase += plane;
+            ++zcur;
         };
 
         // prologue: planes t = 0 .. 2R-1.  Planes t < R and t >= nseg + R

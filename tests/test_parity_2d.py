@@ -94,8 +94,7 @@ def test_fused_runs_bit_identical(oracle, kind, dtype, shape, fusion, n):
                                                            device="cuda")]
         idx = st.run(d, n)
         torch.cuda.synchronize()
-        if fu == 1:
-            assert idx == ridx                  # fused runs report their own index
+        assert idx == ridx
         res[fu] = d[idx].cpu().numpy()
         st.close()
     assert_parity(res[fusion], bufs[ridx], dtype, f"{kind} fused {fusion}")
