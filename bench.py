@@ -228,7 +228,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--attach", action="store_true",
-                    help="run the NCCL-attached (slab) path even at N=1 (a group of one rank)")
+                    help="run the attached (slab) path even at N=1 (a group of one rank)")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="halo exchange for N>1: fused peer stores over CUDA IPC (default) or NCCL send/recv")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
@@ -256,14 +258,18 @@ def main():
     dims = list(wl["dims"])
     dims[-1] *= world                 # weak scaling along the slowest axis
     st = Stencil(wl["kind"], dims, wl["dtype"], variant=args.variant)
-    if world > 1:
-        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(dist_get_id()), dtype=torch.uint8))
-        dist.broadcast(uid, 0)
-        st.attach(bytes(uid.cpu().tolist()), rank, world)
-    elif args.attach:                 # the multi-GPU code path with a group of one
-        st.attach(dist_get_id(), 0, 1)
+    attached = world > 1 or args.attach
+    if attached and args.transport == "nccl":
+        if world > 1:
+            uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                uid.copy_(torch.frombuffer(bytearray(dist_get_id()), dtype=torch.uint8))
+            dist.broadcast(uid, 0)
+            st.attach(bytes(uid.cpu().tolist()), rank, world)
+        else:                         # the multi-GPU code path with a group of one
+            st.attach(dist_get_id(), 0, 1)
+    elif attached:
+        st.attach_p2p(rank, world)
     info = st.info()
     n_in, n_out, n_bufs = st.arity()
     ldims = info["local_dims"][: len(dims)]
@@ -278,6 +284,14 @@ def main():
         bufs = [fields[0], fields[1], torch.zeros_like(fields[0])]
     else:
         bufs = fields + [torch.zeros_like(fields[0]) for _ in range(n_out)]
+    if attached and args.transport == "p2p":
+        def allgather(blob):
+            if world == 1:
+                return [blob]
+            parts = [None] * world
+            dist.all_gather_object(parts, blob)
+            return parts
+        st.p2p_register(bufs, allgather)
     nbytes_buf = bufs[0].numel() * bufs[0].element_size()
     flush = None
     if nbytes_buf * len(bufs) < 2 * L2_BYTES:
@@ -411,7 +425,8 @@ def main():
             "config": {"workload": wl["config"], "kind": wl["kind"], "dims": dims,
                        "local_dims": list(ldims), "iters_per_step": iters,
                        "variant": args.variant,
-                       "parallelism": f"slab{world}" if world > 1 else ("slab1" if args.attach else "1gpu"),
+                       "parallelism": (f"slab{world}" if world > 1 else "slab1") if attached else "1gpu",
+                       "transport": args.transport if attached else None,
                        "l2": "flushed between timed steps" if flush is not None
                        else "inputs larger than L2"},
             "hbm_gbs": achieved * 1.0,

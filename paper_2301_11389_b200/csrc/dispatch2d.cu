@@ -25,13 +25,16 @@ static int sm_count(int device) {
 // the grid (good DRAM row locality, and the 2R rows two neighbouring strips
 // share are read once, from L2, by the second); one wave of tall strips
 // scatters the accesses over ~40 bands and ran 13-30% slower.
-template <class Op, typename T, int VAR>
+// FUSED: the P2P instantiation with the peer halo stores (a separate kernel,
+// so the plain path carries none of its registers or branches).
+template <class Op, typename T, int VAR, bool FUSED = false>
 static cudaError_t launch_k2d(const stencil_s* h, const void* in, void* out, cudaStream_t s,
                               int64_t y_lo, int64_t y_hi) {
     constexpr int R = Op::R;
     constexpr int V = vlen<T>();
     constexpr int kStripH = 24;
-    auto kern = k2d<Op, T, VAR>;
+    if (!FUSED && (h->peer_lo || h->peer_hi)) return launch_k2d<Op, T, VAR, true>(h, in, out, s, y_lo, y_hi);
+    auto kern = k2d<Op, T, VAR, FUSED>;
     constexpr size_t smem = k2d_smem_bytes<T>();
     static bool attr = false;
     if (!attr) {

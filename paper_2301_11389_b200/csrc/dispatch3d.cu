@@ -52,11 +52,12 @@ int sm_count_of(int device) {
     return cached[device];
 }
 
-template <class Op, typename T, int VAR>
+template <class Op, typename T, int VAR, bool FUSED = false>
 static cudaError_t launch_k3d(const stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
                               int64_t z_lo, int64_t z_hi) {
     using L = Layout3<Op, T>;
-    auto kern = k3d<Op, T, VAR>;
+    if (!FUSED && (h->peer_lo || h->peer_hi)) return launch_k3d<Op, T, VAR, true>(h, in, out, s, z_lo, z_hi);
+    auto kern = k3d<Op, T, VAR, FUSED>;
     constexpr size_t smem = L::smem_bytes();
     static int blocks_per_sm = 0;
     if (!blocks_per_sm) {

@@ -101,6 +101,7 @@ static void output_slabs(const stencil_s* h, int64_t* a, int64_t* x0, int64_t* x
 int dist_launches_per_step(const stencil_s* h) {
     int64_t a, x0, x1, b;
     output_slabs(h, &a, &x0, &x1, &b);
+    if (h->dist->p2p) return b > a;    // one launch with fused peer stores
     return (x0 > a) + (x1 > x0) + (b > x1);
 }
 

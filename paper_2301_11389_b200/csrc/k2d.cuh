@@ -152,7 +152,7 @@ constexpr int k2d_threads() { return (kWarps2D + 1) * 32; }
 
 // Grid: x = ceil(ntiles / kWarps2D), y = strips of H output rows covering
 // output rows [y_lo, y_hi) (R <= y_lo, y_hi <= ny - R).
-template <class Op, typename T, int VARIANT>
+template <class Op, typename T, int VARIANT, bool FUSED = false>
 __global__ void __launch_bounds__(k2d_threads())
 k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_hi, int H,
     Coeffs<T, Op::NC> c, PeerOut<T> peer) {
@@ -269,7 +269,6 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
     auto sweep = [&](auto edge_tag) {
         constexpr bool EDGE = decltype(edge_tag)::value;
         T* optr = out + (int64_t)ys * nx + xl;             // running output pointer
-        const bool fused = peer.lo != nullptr || peer.hi != nullptr;
         auto emit = [&](int u, int yrow) {
             T o[V];
             const Win<T, NW, W, R> w{win, u};
@@ -295,7 +294,7 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
                 }
             };
             store(optr);
-            if (fused) {                                   // warp-uniform: halo rows to the peers
+            if constexpr (FUSED) {                         // warp-uniform: halo rows to the peers
                 if (peer.lo && yrow < peer.lo_end) store(peer.lo + (optr - out) + peer.d_lo);
                 if (peer.hi && yrow >= peer.hi_begin) store(peer.hi + (optr - out) + peer.d_hi);
             }

@@ -222,7 +222,7 @@ struct K3Args {
 };
 
 // ------------------------------------------------------------------ kernel
-template <class Op, typename T, int VARIANT>
+template <class Op, typename T, int VARIANT, bool FUSED = false>
 __global__ void __launch_bounds__(k3d_threads(), 1)
 k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<Op, T> args,
     const Coeffs<T, Op::NC> c) {
@@ -294,7 +294,6 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
         for (int p = 0; p < V; ++p) x_el[p] = !x_vec && own && xl + p >= R && xl + p < args.nx - R;
         int64_t obase = ((int64_t)(args.z_lo + zo) * args.ny + y0) * args.nx + xl;
         int64_t zcur = args.z_lo + zo;                     // output plane of the next emit
-        const bool fused = args.peer.lo != nullptr || args.peer.hi != nullptr;
         const int np = nseg + 2 * R;
 
         // element offset of (row warp*RY + r + dy, lane vector + e) in array a's box
@@ -376,7 +375,7 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
                 };
 #pragma unroll
                 for (int k = 0; k < Op::NOUT; ++k) store(args.out[k] + obase + r * args.nx, o[k]);
-                if (fused) {                               // halo planes straight to the peers
+                if constexpr (FUSED) {                     // halo planes straight to the peers
                     if (args.peer.lo && zcur < args.peer.lo_end)
                         store(args.peer.lo + obase + r * args.nx + args.peer.d_lo, o[0]);
                     if (args.peer.hi && zcur >= args.peer.hi_begin)

@@ -139,16 +139,13 @@ static void clear_peer(stencil_s* h) {
     h->peer_lo_end = h->peer_hi_begin = h->peer_d_lo = h->peer_d_hi = 0;
 }
 
-// Launch all slabs of one step; boundary slabs first so the fused halo
-// stores leave as early as possible.
-static int launch_slabs(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s) {
+// One launch over all owned output planes: the halos are already in place
+// (the stream waited for them), and the kernel itself stores the boundary
+// planes into the neighbours, so there is nothing to overlap by splitting.
+static int launch_owned(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s) {
     int64_t a, x0, x1, b;
     dist_output_slabs(h, &a, &x0, &x1, &b);
-    int rc;
-    if (x0 > a && (rc = launch_sweep(h, in, out, s, a, x0))) return rc;
-    if (b > x1 && (rc = launch_sweep(h, in, out, s, x1, b))) return rc;
-    if (x1 > x0 && (rc = launch_sweep(h, in, out, s, x0, x1))) return rc;
-    return ST_OK;
+    return b > a ? launch_sweep(h, in, out, s, a, b) : ST_OK;
 }
 
 // stencil_step on a P2P-attached handle: exchange the input halos by peer
@@ -168,7 +165,7 @@ int p2p_step(stencil_s* h, const void* const* in, void* const* out, cudaStream_t
         if (!ps) return set_error(ST_ESTATE, "input %d not registered with stencil_p2p_import", ai);
         if ((rc = exchange_inputs(h, ps, k, s, done_prev, sig))) return rc;
     }
-    if ((rc = launch_slabs(h, in, out, s))) return rc;
+    if ((rc = launch_owned(h, in, out, s))) return rc;
     p->epoch = sig;
     return write_val(s, p->flags, p->epoch);
 }
@@ -203,7 +200,7 @@ int p2p_run(stencil_s* h, void* const* bufs, int n_iters, cudaStream_t s, int* r
         for (int a = 0; a < k->n_in; ++a) in[a] = bufs[a];
         for (int b = 0; b < k->n_out; ++b) out[b] = bufs[k->n_in + b];
         for (int it = 0; it < n_iters; ++it)
-            if ((rc = launch_slabs(h, in, out, s))) return rc;
+            if ((rc = launch_owned(h, in, out, s))) return rc;
         p->epoch = base + 1;
         if ((rc = write_val(s, p->flags, p->epoch))) return rc;
         *result = k->n_in;
@@ -237,17 +234,11 @@ int p2p_run(stencil_s* h, void* const* bufs, int n_iters, cudaStream_t s, int* r
         h->peer_d_lo = m * plane_elems;
         h->peer_hi_begin = m;                          // my planes [m, m+lo) -> upper's [0, lo)
         h->peer_d_hi = -m * plane_elems;
-        int64_t a, x0, x1, b;
-        dist_output_slabs(h, &a, &x0, &x1, &b);
         const void* in[2];
         void* out[1] = {bufs[io]};
         if (k->iterable == 1) in[0] = bufs[ic];
         else { in[0] = bufs[idx[0]]; in[1] = bufs[ic]; }
-        rc = ST_OK;
-        if (x0 > a) rc = launch_sweep(h, in, out, s, a, x0);
-        if (!rc && b > x1) rc = launch_sweep(h, in, out, s, x1, b);
-        // an interior plane can also be a boundary plane when slabs are thin
-        if (!rc && x1 > x0) rc = launch_sweep(h, in, out, s, x0, x1);
+        rc = launch_owned(h, in, out, s);
         clear_peer(h);
         if (rc) return rc;
         for (int q = 0; q < 2; ++q)
