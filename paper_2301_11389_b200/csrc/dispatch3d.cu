@@ -8,6 +8,7 @@
 #include "internal.h"
 #include "k3d.cuh"
 #include "ktricubic.cuh"
+#include "ktricubic2.cuh"
 
 namespace stb200 {
 
@@ -193,8 +194,47 @@ static cudaError_t launch_tri(const stencil_s* h, const void* const* in, void* c
     return cudaGetLastError();
 }
 
+// fp32: two output rows per warp, flattened equal ranges (ktricubic2.cuh)
+template <int VAR>
+static cudaError_t launch_tri2(const stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
+                               int64_t z_lo, int64_t z_hi) {
+    using L = Tri2Layout;
+    auto kern = ktricubic2<VAR>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
+        attr = true;
+    }
+    const int64_t* ld = h->ldims;
+    if (z_lo < 0) { z_lo = 1; z_hi = ld[2] - 2; }
+    if (z_hi <= z_lo) return cudaSuccess;
+    TmapPack<4> tm;
+    cudaError_t e = make_tmap(&tm.m[0], in[0], h->dtype, ld, L::FBX, L::FBY);
+    for (int a = 1; a < 4 && e == cudaSuccess; ++a) e = make_tmap(&tm.m[a], in[a], h->dtype, ld, L::TX, L::TY);
+    if (e != cudaSuccess) return e;
+    TriArgs<float> args{};
+    args.X = (const float*)in[1];
+    args.Y = (const float*)in[2];
+    args.Z = (const float*)in[3];
+    args.out = (float*)out[0];
+    args.nx = ld[0];
+    args.ny = ld[1];
+    args.z_lo = (int)z_lo;
+    args.nzo = (int)(z_hi - z_lo);
+    args.ntx = (int)((ld[0] + L::TX - 1) / L::TX);
+    args.nty = (int)((ld[1] + L::TY - 1) / L::TY);
+    const int64_t items = (int64_t)args.ntx * args.nty * args.nzo;
+    int64_t grid = sm_count_of(h->device);
+    if (grid > items) grid = items;
+    kern<<<(unsigned)grid, (kTri2Warps + 1) * 32, L::SMEM, s>>>(tm, args);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_tricubic(const stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
                             int64_t a, int64_t b) {
+    static const int old1 = getenv("STB200_TRI1") ? atoi(getenv("STB200_TRI1")) : 0;
+    if (h->dtype == ST_F32 && !old1)
+        return h->variant == ST_PLAIN ? launch_tri2<1>(h, in, out, s, a, b) : launch_tri2<0>(h, in, out, s, a, b);
     if (h->dtype == ST_F64)
         return h->variant == ST_PLAIN ? launch_tri<double, 1>(h, in, out, s, a, b)
                                       : launch_tri<double, 0>(h, in, out, s, a, b);

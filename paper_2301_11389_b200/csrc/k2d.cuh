@@ -203,7 +203,7 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
             const T* src = in + (int64_t)row0 * nx + g_lo;
             for (unsigned r = 0; r < (unsigned)nrows; ++r, src += nx) {
                 const unsigned s = r & (S - 1);
-                if (r >= S) mbar_wait(&empty[s], ((r >> LOG2S) - 1) & 1u);
+                if (r >= S) mbar_wait_backoff<256>(&empty[s], ((r >> LOG2S) - 1) & 1u);
                 mbar_arrive_expect_tx(&full[s], bytes);
                 bulk_g2s(dst0 + s * WS, src, bytes, &full[s]);
             }

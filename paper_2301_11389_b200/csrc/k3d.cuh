@@ -257,7 +257,7 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
                 const int z_first = args.z_lo + zo - R;
                 for (int t = 0; t < nseg + 2 * R; ++t, ++g) {
                     const uint32_t s = g % NS;
-                    if (g >= NS) mbar_wait(&empty[s], (g / NS - 1) & 1u);
+                    if (g >= NS) mbar_wait_backoff<512>(&empty[s], (g / NS - 1) & 1u);
                     mbar_arrive_expect_tx(&full[s], L::tx_bytes());
                     unsigned char* st = smem + (size_t)s * L::stage_bytes();
 #pragma unroll

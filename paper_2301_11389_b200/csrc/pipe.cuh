@@ -49,6 +49,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// Wait used by producer warps: back off between polls (exponentially, up
+// to MAXNS ns) so that a producer waiting for the consumers to free a stage
+// does not take issue slots from the consumer warps of its SM sub-partition.
+template <uint32_t MAXNS>
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+    uint32_t ok, ns = 32;
+    for (;;) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+        if (ok) return;
+        __nanosleep(ns);
+        if (ns < MAXNS) ns *= 2;
+    }
+}
+
 // Bulk copy global -> shared (contiguous, 16-byte aligned, bytes % 16 == 0),
 // completion signalled on `bar` as transaction bytes.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
