@@ -38,6 +38,20 @@ __device__ __forceinline__ void stg_vec(T* p, const T* v) {
     *reinterpret_cast<VT*>(p) = t;
 }
 
+// 16-byte shared-memory store (STS.128).
+template <typename T>
+__device__ __forceinline__ void st_vec_s(T* p, const T* v) { stg_vec(p, v); }
+
+// 16-byte streaming store (st.global.cs: evict-first in L1/L2).
+template <typename T>
+__device__ __forceinline__ void stcs_vec(T* p, const T* v) {
+    using VT = typename VecOf<T>::type;
+    VT t;
+    if constexpr (VecOf<T>::V == 4) { t.x = v[0]; t.y = v[1]; t.z = v[2]; t.w = v[3]; }
+    else { t.x = v[0]; t.y = v[1]; }
+    __stcs(reinterpret_cast<VT*>(p), t);
+}
+
 // Load R consecutive elements starting at p; p is aligned to R*sizeof(T)
 // whenever R*sizeof(T) is 8 or 16 (see the alignment argument in k2d.cuh).
 template <typename T, int R>

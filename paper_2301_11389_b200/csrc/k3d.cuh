@@ -77,6 +77,7 @@ struct Ctx3 {
 // laplacian3d7 / jacobi3d7: a*C + b*(x+1 + x-1 + y+1 + y-1 + z+1 + z-1)
 template <typename T> struct OpLap7 {
     static constexpr int R = 1, NA = 1, QA = 0, NOUT = 1, NC = 2;
+    static constexpr bool BULK = false;             // S7 through bulk stores (measured)
     __host__ __device__ static constexpr int box(int) { return BOX_XY; }
     template <class Cx>
     __device__ __forceinline__ static void point(const Cx& x, int p, const Coeffs<T, NC>& c, T* o) {
@@ -92,6 +93,7 @@ template <typename T> struct OpLap7 {
 // wave13pt: m0*cur + m1*(6 at distance 1) + m2*(6 at distance 2) - prev
 template <typename T> struct OpWave13 {
     static constexpr int R = 2, NA = 2, QA = 1, NOUT = 1, NC = 3;
+    static constexpr bool BULK = true;             // S7 through bulk stores (measured)
     __host__ __device__ static constexpr int box(int a) { return a == 0 ? BOX_C : BOX_XY; }  // prev, cur
     template <class Cx>
     __device__ __forceinline__ static void point(const Cx& x, int p, const Coeffs<T, NC>& c, T* o) {
@@ -114,6 +116,7 @@ template <typename T> struct OpWave13 {
 // gradient: (ax*(x+1 - x-1), ay*(y+1 - y-1), az*(z+1 - z-1))
 template <typename T> struct OpGradient {
     static constexpr int R = 1, NA = 1, QA = 0, NOUT = 3, NC = 3;
+    static constexpr bool BULK = false;             // S7 through bulk stores (measured)
     __host__ __device__ static constexpr int box(int) { return BOX_XY; }
     template <class Cx>
     __device__ __forceinline__ static void point(const Cx& x, int p, const Coeffs<T, NC>& c, T* o) {
@@ -126,6 +129,7 @@ template <typename T> struct OpGradient {
 // divergence: ax*(u[x+1]-u[x-1]) + ay*(v[y+1]-v[y-1]) + az*(w[z+1]-w[z-1])
 template <typename T> struct OpDivergence {
     static constexpr int R = 1, NA = 3, QA = 2, NOUT = 1, NC = 3;
+    static constexpr bool BULK = false;             // S7 through bulk stores (measured)
     __host__ __device__ static constexpr int box(int a) {  // u, v, w
         return a == 0 ? BOX_X : a == 1 ? BOX_Y : BOX_C;
     }
@@ -166,10 +170,18 @@ struct Layout3 {
         for (int a = 0; a < Op::NA; ++a) s += box_bytes(a);
         return s;
     }
-    // stages: as many as fit in ~200 KB (one CTA per SM), at least 2R+2
-    static constexpr int NS_FIT = (200 * 1024) / stage_bytes();
+    // output staging for the bulk (TMA) stores: one TX-wide row per
+    // (warp, row, output), after the ring
+    static constexpr int OUT_ROW = TX * (int)sizeof(T);
+    static constexpr int out_bytes() { return kWarps3D * RY * Op::NOUT * OUT_ROW; }
+    // stages: as many as fit in ~200 KB with the staging (one CTA per SM), at least 2R+2
+    static constexpr int NS_FIT = (200 * 1024 - out_bytes()) / stage_bytes();
     static constexpr int NS = NS_FIT > 8 ? 8 : (NS_FIT < 2 * R + 2 ? 2 * R + 2 : NS_FIT);
-    static constexpr size_t smem_bytes() { return (size_t)NS * stage_bytes() + 2 * NS * sizeof(uint64_t); }
+    static constexpr size_t out_off() { return (size_t)NS * stage_bytes(); }
+    static constexpr size_t smem_bytes() {
+        return out_off() + out_bytes() + 2 * NS * sizeof(uint64_t);
+    }
+    static_assert(smem_bytes() <= 232448, "k3d shared memory over the 227 KB per-CTA limit");
 };
 constexpr int k3d_threads() { return (kWarps3D + 1) * 32; }
 
@@ -219,6 +231,7 @@ struct K3Args {
     int zsplit, zc, m;     // LockIter: z parts per column, chunk planes, items per CTA
     PeerOut<T> peer;       // fused halo stores of out[0] (P2P multi-GPU), off when null
     int dbg;               // experiment switches (0 in production)
+    int bulk;              // S7 through bulk (TMA) stores from a staging row, else STG.128
 };
 
 // ------------------------------------------------------------------ kernel
@@ -231,7 +244,7 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
     constexpr int RY = L::RY, NS = L::NS, NQ = 2 * R + 1;
 
     extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NS * L::stage_bytes());
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::out_off() + L::out_bytes());
     uint64_t* empty = full + NS;
     const int warp = threadIdx.x >> 5, lane = lane_id();
 
@@ -277,6 +290,7 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
     for (int t = 0; t < Op::NC; ++t) cr.c[t] = c.c[t];
     const bool lane0 = lane == 0, lane31 = lane == 31;
     T q[RY][NQ][V];                                        // z queue per row
+    T* out_stage = reinterpret_cast<T*>(smem + L::out_off()) + (size_t)warp * RY * Op::NOUT * TX;
     uint32_t g = 0;
     const int64_t plane = args.nx * args.ny;
 
@@ -293,6 +307,10 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
 #pragma unroll
         for (int p = 0; p < V; ++p) x_el[p] = !x_vec && own && xl + p >= R && xl + p < args.nx - R;
         int64_t obase = ((int64_t)(args.z_lo + zo) * args.ny + y0) * args.nx + xl;
+        // 16-byte aligned interior span [xa, xb) of the tile's rows (bulk stores)
+        const int64_t x0 = (int64_t)tx * TX;
+        const int64_t xa = ((x0 > R ? x0 : R) + V - 1) / V * V;
+        const int64_t xb = ((x0 + TX < args.nx - R ? x0 + TX : args.nx - R)) / V * V;
         int64_t zcur = args.z_lo + zo;                     // output plane of the next emit
         const int np = nseg + 2 * R;
 
@@ -373,14 +391,43 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
                     for (int p = 0; p < V; ++p)
                         if (row_ok && x_el[p]) op[p] = ov[p];
                 };
+                // S7 store.  Whole interior vectors go to the warp's staging row
+                // and leave as one bulk copy per row (below); lanes with a
+                // partial vector (grid edge) store their interior elements.
+                if (args.bulk) {
+                    if (r == 0) bulk_wait_read(lane0);           // staging rows free again
 #pragma unroll
-                for (int k = 0; k < Op::NOUT; ++k) store(args.out[k] + obase + r * args.nx, o[k]);
+                    for (int k = 0; k < Op::NOUT; ++k) {
+                        if (x_vec) st_vec_s(out_stage + (r * Op::NOUT + k) * TX + lane * V, o[k]);
+#pragma unroll
+                        for (int p = 0; p < V; ++p)
+                            if (row_ok && x_el[p]) args.out[k][obase + r * args.nx + p] = o[k][p];
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < Op::NOUT; ++k) store(args.out[k] + obase + r * args.nx, o[k]);
+                }
                 if constexpr (FUSED) {                     // halo planes straight to the peers
                     if (args.peer.lo && zcur < args.peer.lo_end)
                         store(args.peer.lo + obase + r * args.nx + args.peer.d_lo, o[0]);
                     if (args.peer.hi && zcur >= args.peer.hi_begin)
                         store(args.peer.hi + obase + r * args.nx + args.peer.d_hi, o[0]);
                 }
+            }
+            // one bulk copy (cp.async.bulk, the TMA engine) per interior row
+            // segment and output: the stores leave the LSU queue
+            if (args.bulk) fence_proxy_async_smem();
+            __syncwarp();
+            if (args.bulk && lane0 && xb > xa) {
+#pragma unroll
+                for (int r = 0; r < RY; ++r) {
+                    if (y0 + r < R || y0 + r >= args.ny - R) continue;
+#pragma unroll
+                    for (int k = 0; k < Op::NOUT; ++k)
+                        bulk_s2g(args.out[k] + (obase - lane * V) + r * args.nx + (xa - x0),
+                                 out_stage + (r * Op::NOUT + k) * TX + (xa - x0), (uint32_t)((xb - xa) * sizeof(T)));
+                }
+                bulk_commit();
             }
             release(gg);
             obase += plane;
@@ -417,6 +464,7 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
         }
         g += np;
     }
+    bulk_wait_all(lane0);
 }
 
 }  // namespace stb200

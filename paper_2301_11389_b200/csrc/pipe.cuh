@@ -77,6 +77,26 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// Bulk copy shared -> global (contiguous, 16-byte aligned, bytes % 16 ==
+// 0) in the issuing thread's bulk group; the source may be reused once
+// bulk_wait_read has returned in the same thread.
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// Thread t's earlier bulk stores have finished reading shared memory; then
+// the warp may overwrite the staging rows.
+__device__ __forceinline__ void bulk_wait_read(bool t) {
+    if (t) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncwarp();
+}
+__device__ __forceinline__ void bulk_wait_all(bool t) {
+    if (t) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+}
+
 // L2 eviction-first policy for streamed data read exactly once.
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;

@@ -3,6 +3,7 @@
 // ceiling each stencil's traffic mix can expect.  nvcc -gencode
 // arch=compute_100a,code=sm_100a -O3 -o rwmix tools/rwmix.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 template <int NR, int NW>
 __global__ void mix(const float4* __restrict__ a, const float4* __restrict__ b, const float4* __restrict__ c,
@@ -16,24 +17,26 @@ __global__ void mix(const float4* __restrict__ a, const float4* __restrict__ b, 
         if (NW > 2) z[i] = v;
     }
 }
+static int g_blocks_per_sm = 8;
 template <int NR, int NW>
 void run(float4** p, size_t n, const char* name) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    for (int i = 0; i < 3; ++i) mix<NR, NW><<<nsm * 8, 512>>>(p[0], p[1], p[2], p[3], p[4], p[5], n);
+    for (int i = 0; i < 3; ++i) mix<NR, NW><<<nsm * g_blocks_per_sm, 512>>>(p[0], p[1], p[2], p[3], p[4], p[5], n);
     cudaEventRecord(e0);
     const int it = 20;
-    for (int i = 0; i < it; ++i) mix<NR, NW><<<nsm * 8, 512>>>(p[0], p[1], p[2], p[3], p[4], p[5], n);
+    for (int i = 0; i < it; ++i) mix<NR, NW><<<nsm * g_blocks_per_sm, 512>>>(p[0], p[1], p[2], p[3], p[4], p[5], n);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     printf("\"%s\": %.1f, ", name, (double)(NR + NW) * n * 16 * it / (ms / 1e3) / 1e9);
 }
-int main() {
+int main(int argc, char** argv) {
+    if (argc > 1) g_blocks_per_sm = atoi(argv[1]);   // 1 = 16 warps per SM (the k3d occupancy)
     const size_t n = (512ull << 20) / 16;      // 512 MiB per array
     float4* p[6];
     for (int i = 0; i < 6; ++i) { cudaMalloc(&p[i], n * 16); cudaMemset(p[i], 0, n * 16); }
-    printf("{\"GBps_512MiB_arrays\": {");
+    printf("{\"blocks_per_sm\": %d, \"GBps_512MiB_arrays\": {", g_blocks_per_sm);
     run<1, 1>(p, n, "1R1W");
     run<2, 1>(p, n, "2R1W");
     run<3, 1>(p, n, "3R1W");
