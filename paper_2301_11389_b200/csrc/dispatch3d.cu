@@ -4,6 +4,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <cstring>
 
 #include "internal.h"
 #include "k3d.cuh"
@@ -109,9 +110,10 @@ static cudaError_t launch_k3d(const stencil_s* h, const void* const* in, void* c
     args.zc = dbg_zc > 0 ? dbg_zc : (Op::R == 1 && Op::NA == 1 && Op::NOUT == 1) ? 6 : 64;
     static const int dbg = getenv("STB200_DBG") ? atoi(getenv("STB200_DBG")) : 0;
     args.dbg = dbg;
-    // bulk stores (k3d.cuh S7): measured per kind; STB200_BULK=0/1 overrides
-    static const int bulk_env = getenv("STB200_BULK") ? atoi(getenv("STB200_BULK")) : -1;
-    args.bulk = bulk_env >= 0 ? bulk_env : Op::BULK;
+    // S7 store path (k3d.cuh): the kind's measured choice;
+    // STB200_STG=1 forces plain STG stores (A/B experiments)
+    static const int stg_env = getenv("STB200_STG") ? atoi(getenv("STB200_STG")) : 0;
+    args.store = stg_env ? ST_STG : Op::STORE;
     Coeffs<T, Op::NC> c{};
     for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)h->coeffs[t];
     kern<<<(unsigned)grid, k3d_threads(), smem, s>>>(tm, args, c);

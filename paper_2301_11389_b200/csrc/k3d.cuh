@@ -40,6 +40,13 @@ namespace stb200 {
 
 constexpr int kWarps3D = 15;      // consumer warps per CTA (+1 producer = 16 warps, one CTA per SM)
 
+// S7 store paths: STG.128 from the lanes, or per-warp bulk copies of
+// staged rows (cp.async.bulk).  (A third one, one TMA tensor store per
+// output per CTA tile plane behind a named barrier, measured 2x slower on
+// gradient; TMA tensor stores also fault on negative box coordinates, so
+// the lower boundary ring has to be inside the box: DESIGN.md §5.2.)
+enum StorePath { ST_STG = 0, ST_BULK = 1 };
+
 // Staged-box shapes: which halos an array's stencil needs.
 enum BoxKind { BOX_XY = 0, BOX_X = 1, BOX_Y = 2, BOX_C = 3 };
 __host__ __device__ constexpr bool box_xh(int b) { return b == BOX_XY || b == BOX_X; }
@@ -77,7 +84,7 @@ struct Ctx3 {
 // laplacian3d7 / jacobi3d7: a*C + b*(x+1 + x-1 + y+1 + y-1 + z+1 + z-1)
 template <typename T> struct OpLap7 {
     static constexpr int R = 1, NA = 1, QA = 0, NOUT = 1, NC = 2;
-    static constexpr bool BULK = false;             // S7 through bulk stores (measured)
+    static constexpr int STORE = ST_STG;            // S7 store path (measured)
     __host__ __device__ static constexpr int box(int) { return BOX_XY; }
     template <class Cx>
     __device__ __forceinline__ static void point(const Cx& x, int p, const Coeffs<T, NC>& c, T* o) {
@@ -93,7 +100,7 @@ template <typename T> struct OpLap7 {
 // wave13pt: m0*cur + m1*(6 at distance 1) + m2*(6 at distance 2) - prev
 template <typename T> struct OpWave13 {
     static constexpr int R = 2, NA = 2, QA = 1, NOUT = 1, NC = 3;
-    static constexpr bool BULK = true;             // S7 through bulk stores (measured)
+    static constexpr int STORE = ST_BULK;           // S7 store path (measured)
     __host__ __device__ static constexpr int box(int a) { return a == 0 ? BOX_C : BOX_XY; }  // prev, cur
     template <class Cx>
     __device__ __forceinline__ static void point(const Cx& x, int p, const Coeffs<T, NC>& c, T* o) {
@@ -116,7 +123,7 @@ template <typename T> struct OpWave13 {
 // gradient: (ax*(x+1 - x-1), ay*(y+1 - y-1), az*(z+1 - z-1))
 template <typename T> struct OpGradient {
     static constexpr int R = 1, NA = 1, QA = 0, NOUT = 3, NC = 3;
-    static constexpr bool BULK = false;             // S7 through bulk stores (measured)
+    static constexpr int STORE = ST_STG;            // S7 store path (measured)
     __host__ __device__ static constexpr int box(int) { return BOX_XY; }
     template <class Cx>
     __device__ __forceinline__ static void point(const Cx& x, int p, const Coeffs<T, NC>& c, T* o) {
@@ -129,7 +136,7 @@ template <typename T> struct OpGradient {
 // divergence: ax*(u[x+1]-u[x-1]) + ay*(v[y+1]-v[y-1]) + az*(w[z+1]-w[z-1])
 template <typename T> struct OpDivergence {
     static constexpr int R = 1, NA = 3, QA = 2, NOUT = 1, NC = 3;
-    static constexpr bool BULK = false;             // S7 through bulk stores (measured)
+    static constexpr int STORE = ST_STG;            // S7 store path (measured)
     __host__ __device__ static constexpr int box(int a) {  // u, v, w
         return a == 0 ? BOX_X : a == 1 ? BOX_Y : BOX_C;
     }
@@ -173,7 +180,9 @@ struct Layout3 {
     // output staging for the bulk (TMA) stores: one TX-wide row per
     // (warp, row, output), after the ring
     static constexpr int OUT_ROW = TX * (int)sizeof(T);
-    static constexpr int out_bytes() { return kWarps3D * RY * Op::NOUT * OUT_ROW; }
+    static constexpr int out_bytes() {
+        return Op::STORE == ST_BULK ? kWarps3D * RY * Op::NOUT * OUT_ROW : 0;
+    }
     // stages: as many as fit in ~200 KB with the staging (one CTA per SM), at least 2R+2
     static constexpr int NS_FIT = (200 * 1024 - out_bytes()) / stage_bytes();
     static constexpr int NS = NS_FIT > 8 ? 8 : (NS_FIT < 2 * R + 2 ? 2 * R + 2 : NS_FIT);
@@ -231,7 +240,7 @@ struct K3Args {
     int zsplit, zc, m;     // LockIter: z parts per column, chunk planes, items per CTA
     PeerOut<T> peer;       // fused halo stores of out[0] (P2P multi-GPU), off when null
     int dbg;               // experiment switches (0 in production)
-    int bulk;              // S7 through bulk (TMA) stores from a staging row, else STG.128
+    int store;             // S7 path used (StorePath; the kind's compiled path or ST_STG)
 };
 
 // ------------------------------------------------------------------ kernel
@@ -242,6 +251,7 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
     using L = Layout3<Op, T>;
     constexpr int R = Op::R, NA = Op::NA, V = L::V, TX = L::TX, TY = L::TY;
     constexpr int RY = L::RY, NS = L::NS, NQ = 2 * R + 1;
+    constexpr bool BULK = Op::STORE == ST_BULK && !FUSED;   // bulk-store path compiled in (S7)
 
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::out_off() + L::out_bytes());
@@ -356,10 +366,26 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
 #pragma unroll
                             for (int k = 0; k < R; ++k) x.xw[a][R + V + k] = shfl_down(v[k], 1);
                             // warp edge (%out_of_range): the
-                            // fallback read of the staged neighbour sector,
-                            // predicated (no branch, no select)
-                            lds_pred<T, R>(lane0, b + off(a, r, 0, -R), &x.xw[a][0]);
-                            lds_pred<T, R>(lane31, b + off(a, r, 0, V), &x.xw[a][R + V]);
+                            // fallback read of the staged neighbour sector, one
+                            // load whose address is lane 0's (x0-R..x0-1) or the
+                            // others' (x0+TX..x0+TX+R-1: lane 31's), then selects
+                            T e[R];
+                            {
+                                const T* pe = b + (warp * RY + r + (box_yh(Op::box(a)) ? R : 0)) * L::bx(a) +
+                                              L::padx(a) + (lane0 ? -R : TX);
+                                if constexpr (R == 2 && sizeof(T) == 4) {
+                                    const float2 t2 = *reinterpret_cast<const float2*>(pe);
+                                    e[0] = t2.x; e[1] = t2.y;
+                                } else {
+#pragma unroll
+                                    for (int k = 0; k < R; ++k) e[k] = pe[k];
+                                }
+                            }
+#pragma unroll
+                            for (int k = 0; k < R; ++k) {
+                                x.xw[a][k] = lane0 ? e[k] : x.xw[a][k];
+                                x.xw[a][R + V + k] = lane31 ? e[k] : x.xw[a][R + V + k];
+                            }
                         } else {                          // PLAIN: neighbours' elements from smem
 #pragma unroll
                             for (int k = 0; k < R; ++k) x.xw[a][k] = b[off(a, r, 0, k - R)];
@@ -394,7 +420,7 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
                 // S7 store.  Whole interior vectors go to the warp's staging row
                 // and leave as one bulk copy per row (below); lanes with a
                 // partial vector (grid edge) store their interior elements.
-                if (args.bulk) {
+                if (BULK && args.store == ST_BULK) {
                     if (r == 0) bulk_wait_read(lane0);           // staging rows free again
 #pragma unroll
                     for (int k = 0; k < Op::NOUT; ++k) {
@@ -416,9 +442,11 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
             }
             // one bulk copy (cp.async.bulk, the TMA engine) per interior row
             // segment and output: the stores leave the LSU queue
-            if (args.bulk) fence_proxy_async_smem();
-            __syncwarp();
-            if (args.bulk && lane0 && xb > xa) {
+            if (BULK && args.store == ST_BULK) {
+                fence_proxy_async_smem();
+                __syncwarp();
+            }
+            if (BULK && args.store == ST_BULK && lane0 && xb > xa) {
 #pragma unroll
                 for (int r = 0; r < RY; ++r) {
                     if (y0 + r < R || y0 + r >= args.ny - R) continue;
@@ -464,7 +492,7 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
         }
         g += np;
     }
-    bulk_wait_all(lane0);
+    if (BULK) bulk_wait_all(lane0);
 }
 
 }  // namespace stb200
