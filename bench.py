@@ -227,6 +227,8 @@ def main():
     ap.add_argument("--variant", default="shuffle", choices=["shuffle", "plain"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-lanes", type=int, default=4,
+                    help="e2e pipeline depth: handles / device workspaces / streams in flight (1 = serial)")
     ap.add_argument("--attach", action="store_true",
                     help="run the attached (slab) path even at N=1 (a group of one rank)")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
@@ -385,30 +387,67 @@ def main():
         variants[other] = pts_all * iters * len(o_ev) / (float(o_ms.item()) / 1e3) / 1e9
         st.set_variant(args.variant)
 
-    # ---- end to end through the C ABI with HOST buffers
+    # ---- end to end through the C ABI with HOST buffers: every step copies
+    # its inputs from pinned host memory, runs, and copies its result back.
+    # Unattached runs pipeline consecutive steps on two streams (two handles,
+    # two device workspaces, stencil_run_host_async): step k's copies overlap
+    # step k+1's sweeps; attached (multi-rank) runs are serial
+    # (stencil_run_host, one step at a time).
     e2e = None
     if not args.no_e2e:
         n_up = 1 if n_bufs == 2 else (2 if wl["kind"] == "wave13pt" else n_in)
         n_down = 1 if n_bufs in (2, 3) else n_out
         h_in = [bufs[a].cpu().pin_memory() for a in range(n_up)]
         h_out = [torch.empty_like(h_in[0]).pin_memory() for _ in range(n_down)]
-        st.run_host(h_in, h_out, bufs, iters, stream)       # warm-up
-        e_ms = []
-        for _ in range(max(2, min(args.steps, 3))):
-            if world > 1:
-                dist.barrier()
+        pipelined = not attached and args.e2e_lanes > 1
+        if pipelined:
+            lanes = [(st, bufs, h_out, stream)]
+            for _ in range(args.e2e_lanes - 1):
+                lanes.append((Stencil(wl["kind"], dims, wl["dtype"], variant=args.variant),
+                              [torch.empty_like(b) for b in bufs],
+                              [torch.empty_like(h_in[0]).pin_memory() for _ in range(n_down)],
+                              torch.cuda.Stream()))
+            for hh, bb, ho, ss in lanes:                   # warm-up (graph capture) per lane
+                hh.run_host(h_in, ho, bb, iters, ss)
+            n_e = max(2 * len(lanes), min(args.steps, 4 * len(lanes)))
+            torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            st.run_host(h_in, h_out, bufs, iters, stream)
+            for _, _, _, ss in lanes[1:]:
+                ss.wait_event(a)
+            for k in range(n_e):
+                hh, bb, ho, ss = lanes[k % len(lanes)]
+                hh.run_host_async(h_in, ho, bb, iters, ss)
+            for _, _, _, ss in lanes[1:]:
+                j = torch.cuda.Event()
+                j.record(ss)
+                stream.wait_event(j)
             b.record(stream)
             torch.cuda.synchronize()
-            e_ms.append(a.elapsed_time(b))
-        et = torch.tensor([sum(e_ms) / len(e_ms)], dtype=torch.float64, device="cuda")
+            et = torch.tensor([a.elapsed_time(b) / n_e], dtype=torch.float64, device="cuda")
+            for hh, _, _, _ in lanes[1:]:
+                hh.close()
+            del lanes
+        else:
+            st.run_host(h_in, h_out, bufs, iters, stream)       # warm-up
+            e_ms = []
+            for _ in range(max(2, min(args.steps, 3))):
+                if world > 1:
+                    dist.barrier()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                st.run_host(h_in, h_out, bufs, iters, stream)
+                b.record(stream)
+                torch.cuda.synchronize()
+                e_ms.append(a.elapsed_time(b))
+            et = torch.tensor([sum(e_ms) / len(e_ms)], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e = {"value": pts_all * iters / (float(et.item()) / 1e3) / 1e9, "unit": "Gpoints/s",
                "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() for x in h_in)),
-               "d2h_bytes_per_step": int(sum(x.numel() * x.element_size() for x in h_out))}
+               "d2h_bytes_per_step": int(sum(x.numel() * x.element_size() for x in h_out)),
+               "mode": f"{args.e2e_lanes}-stream pipeline (copies of one step overlap the sweeps of others)"
+                       if pipelined else "serial (one step at a time)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

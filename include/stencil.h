@@ -180,6 +180,15 @@ int stencil_run(stencil_t h, void* const* bufs, int n_iters, void* stream, int* 
 int stencil_run_host(stencil_t h, const void* const* host_in, void* const* host_out,
                      void* const* dev_bufs, int n_iters, void* stream);
 
+/* stencil_run_host without the final synchronisation: the H2D copies, the
+ * run and the D2H copies are only enqueued on `stream` (completion is the
+ * caller's stream sync or event).  Host buffers must be pinned for the
+ * copies to be asynchronous, and must stay valid until the stream reaches
+ * them.  With two handles, two device workspaces and two streams, the
+ * copies of one run overlap the sweeps of the other (bench.py e2e). */
+int stencil_run_host_async(stencil_t h, const void* const* host_in, void* const* host_out,
+                           void* const* dev_bufs, int n_iters, void* stream);
+
 int stencil_destroy(stencil_t h);
 
 /* Thread-local description of the last failure on this thread. */

@@ -25,7 +25,7 @@ STATUS = {0: "ST_OK", -1: "ST_EARG", -2: "ST_EUNSUPPORTED", -3: "ST_EALIGN",
 
 # Every symbol include/stencil.h declares (checked by tests/test_abi.py).
 EXPORTS = ["stencil_create", "stencil_set_variant", "stencil_get_variant", "stencil_set_fusion", "stencil_arity",
-           "stencil_info", "stencil_step", "stencil_step_range", "stencil_run", "stencil_run_host",
+           "stencil_info", "stencil_step", "stencil_step_range", "stencil_run", "stencil_run_host", "stencil_run_host_async",
            "stencil_destroy", "stencil_last_error", "stencil_version", "stencil_slab_plan",
            "stencil_dist_get_id", "stencil_dist_attach", "stencil_dist_attach_host",
            "stencil_dist_attach_p2p", "stencil_p2p_export", "stencil_p2p_import"]
@@ -73,6 +73,7 @@ def lib():
         L.stencil_step_range.argtypes = [vp, vpp, vpp, ctypes.c_int64, ctypes.c_int64, vp]
         L.stencil_run.argtypes = [vp, vpp, ctypes.c_int, vp, ip]
         L.stencil_run_host.argtypes = [vp, vpp, vpp, vpp, ctypes.c_int, vp]
+        L.stencil_run_host_async.argtypes = [vp, vpp, vpp, vpp, ctypes.c_int, vp]
         L.stencil_destroy.argtypes = [vp]
         L.stencil_last_error.restype = ctypes.c_char_p
         L.stencil_version.restype = ctypes.c_char_p
@@ -203,6 +204,13 @@ class Stencil:
         hout = (ctypes.c_void_p * len(host_outs))(*[hp(a) for a in host_outs])
         _check(lib().stencil_run_host(self._h, hin, hout, _ptrs(dev_bufs), int(n_iters),
                                       _stream(stream)), "stencil_run_host")
+
+    def run_host_async(self, host_ins, host_outs, dev_bufs, n_iters: int, stream=None):
+        """run_host without the final synchronisation (pinned host buffers)."""
+        hin = (ctypes.c_void_p * len(host_ins))(*[a.data_ptr() for a in host_ins])
+        hout = (ctypes.c_void_p * len(host_outs))(*[a.data_ptr() for a in host_outs])
+        _check(lib().stencil_run_host_async(self._h, hin, hout, _ptrs(dev_bufs), int(n_iters),
+                                            _stream(stream)), "stencil_run_host_async")
 
     def attach(self, uid: bytes, rank: int, nranks: int):
         _check(lib().stencil_dist_attach(self._h, uid, rank, nranks), "stencil_dist_attach")

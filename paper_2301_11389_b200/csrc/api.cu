@@ -451,8 +451,8 @@ extern "C" int stencil_run(stencil_t h, void* const* bufs, int n_iters, void* st
     return ST_OK;
 }
 
-extern "C" int stencil_run_host(stencil_t h, const void* const* host_in, void* const* host_out,
-                                void* const* dev_bufs, int n_iters, void* stream) {
+extern "C" int stencil_run_host_async(stencil_t h, const void* const* host_in, void* const* host_out,
+                                      void* const* dev_bufs, int n_iters, void* stream) {
     if (!h || !host_in || !host_out || !dev_bufs) return set_error(ST_EARG, "null argument");
     cudaSetDevice(h->device);
     cudaStream_t s = (cudaStream_t)stream;
@@ -473,7 +473,14 @@ extern "C" int stencil_run_host(stencil_t h, const void* const* host_in, void* c
                                         cudaMemcpyDeviceToHost, s);
         if (e != cudaSuccess) return set_error(ST_ECUDA, "D2H copy: %s", cudaGetErrorString(e));
     }
-    cudaError_t e = cudaStreamSynchronize(s);
+    return ST_OK;
+}
+
+extern "C" int stencil_run_host(stencil_t h, const void* const* host_in, void* const* host_out,
+                                void* const* dev_bufs, int n_iters, void* stream) {
+    const int rc = stencil_run_host_async(h, host_in, host_out, dev_bufs, n_iters, stream);
+    if (rc) return rc;
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
     if (e != cudaSuccess) return set_error(ST_ECUDA, "sync: %s", cudaGetErrorString(e));
     return ST_OK;
 }

@@ -1,10 +1,7 @@
-set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+# Round check: smoke, all GPU tests, default bench (+ reference arm), all-workload summary.
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke $?
-timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo pytest $?
-tail -3 gpurun_out/pytest_gpu.log
+timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo pytest $?; tail -2 gpurun_out/pytest_gpu.log
 timeout 600 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo bench $?
 cat gpurun_out/bench_default.json
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2>&1; echo ref $?
-bash tools/bench_all.sh > gpurun_out/bench_all.txt 2>&1
-cat gpurun_out/bench_all.txt
+bash tools/bench_all.sh > gpurun_out/bench_all.txt 2>&1; cat gpurun_out/bench_all.txt
