@@ -12,7 +12,8 @@ import ctypes
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libstencil_b200.so")
+# STB200_LIB: an experiment build (build.build_experiment) for A/B runs
+LIB_PATH = os.environ.get("STB200_LIB") or os.path.join(PKG, "libstencil_b200.so")
 
 KINDS = {"jacobi2d5": 1, "jacobi2d9": 2, "gaussblur5x5": 3, "gameoflife": 4,
          "laplacian3d7": 5, "jacobi3d7": 6, "wave13pt": 7, "divergence": 8,

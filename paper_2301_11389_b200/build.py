@@ -36,11 +36,11 @@ def _deps_mtime() -> float:
     return max(os.path.getmtime(f) for f in files)
 
 
-def _compile(src: str) -> str:
+def _compile(src: str, bdir: str = BUILD, defines: tuple = ()) -> str:
     unit = os.path.splitext(os.path.basename(src))[0]
-    obj = os.path.join(BUILD, unit + ".o")
-    log = os.path.join(BUILD, f"ptxas_{unit}.log")
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
+    obj = os.path.join(bdir, unit + ".o")
+    log = os.path.join(bdir, f"ptxas_{unit}.log")
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
     p = subprocess.run(cmd, capture_output=True, text=True)
     with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + p.stdout + p.stderr)
@@ -48,6 +48,13 @@ def _compile(src: str) -> str:
         sys.stderr.write(p.stderr)
         raise RuntimeError(f"nvcc failed on {unit} (see {log})")
     return obj
+
+
+def _link(objs, lib: str) -> str:
+    tmp = lib + f".tmp{os.getpid()}"
+    subprocess.check_call([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-ldl"])
+    os.replace(tmp, lib)
+    return lib
 
 
 def build(force: bool = False, jobs: int | None = None) -> str:
@@ -58,12 +65,23 @@ def build(force: bool = False, jobs: int | None = None) -> str:
     jobs = jobs or min(len(srcs), os.cpu_count() or 4)
     with cf.ThreadPoolExecutor(jobs) as ex:
         objs = list(ex.map(_compile, srcs))
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-ldl"]
-    subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    return _link(objs, LIB)
+
+
+def build_experiment(name: str, defines: tuple) -> str:
+    """A/B builds: the same sources with extra -D flags into
+    expbuild/<name>/libstencil_b200.so (git-ignored, travels with gpurun; load
+    it with STB200_LIB=<path>)."""
+    bdir = os.path.join(ROOT, "expbuild", name)
+    os.makedirs(bdir, exist_ok=True)
+    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    with cf.ThreadPoolExecutor(min(len(srcs), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(lambda f: _compile(f, bdir, defines), srcs))
+    return _link(objs, os.path.join(bdir, "libstencil_b200.so"))
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv))
+    if len(sys.argv) > 2 and sys.argv[1] == "--exp":   # --exp NAME DEFINE...
+        print(build_experiment(sys.argv[2], tuple(sys.argv[3:])))
+    else:
+        print(build(force="--force" in sys.argv))

@@ -243,6 +243,12 @@ struct K3Args {
     int store;             // S7 path used (StorePath; the kind's compiled path or ST_STG)
 };
 
+// Experiment switches (build.build_experiment): 1 = interior-warp rows take
+// a uniform STG.128-only branch (measured slower: DESIGN.md §5.2).
+#ifndef STB200_XIN
+#define STB200_XIN 0
+#endif
+
 // ------------------------------------------------------------------ kernel
 template <class Op, typename T, int VARIANT, bool FUSED = false>
 __global__ void __launch_bounds__(k3d_threads(), 1)
@@ -316,6 +322,12 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
         bool x_el[V];
 #pragma unroll
         for (int p = 0; p < V; ++p) x_el[p] = !x_vec && own && xl + p >= R && xl + p < args.nx - R;
+        // warp-uniform: every lane holds a whole interior vector (all but the
+        // grid-edge tiles); their rows take the STG.128-only store path
+        const bool xin = __all_sync(FULL, x_vec);
+        bool rows_ok[RY];                                  // output row inside the grid interior
+#pragma unroll
+        for (int r = 0; r < RY; ++r) rows_ok[r] = y0 + r >= R && y0 + r < args.ny - R;
         int64_t obase = ((int64_t)(args.z_lo + zo) * args.ny + y0) * args.nx + xl;
         // 16-byte aligned interior span [xa, xb) of the tile's rows (bulk stores)
         const int64_t x0 = (int64_t)tx * TX;
@@ -410,12 +422,16 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
 #pragma unroll
                     for (int k = 0; k < Op::NOUT; ++k) o[k][p] = res[k];
                 }
-                const bool row_ok = y0 + r >= R && y0 + r < args.ny - R;
+                const bool row_ok = rows_ok[r];
                 auto store = [&](T* op, const T* ov) {
-                    if (row_ok && x_vec) stg_vec(op, ov);
+                    if (STB200_XIN && xin && row_ok) {      // uniform branch: interior warp row
+                        stg_vec(op, ov);
+                    } else {
+                        if (row_ok && x_vec) stg_vec(op, ov);
 #pragma unroll
-                    for (int p = 0; p < V; ++p)
-                        if (row_ok && x_el[p]) op[p] = ov[p];
+                        for (int p = 0; p < V; ++p)
+                            if (row_ok && x_el[p]) op[p] = ov[p];
+                    }
                 };
                 // S7 store.  Whole interior vectors go to the warp's staging row
                 // and leave as one bulk copy per row (below); lanes with a
