@@ -107,7 +107,9 @@ static cudaError_t launch_k3d(const stencil_s* h, const void* const* in, void* c
     // chunk depth (measured): the single-array radius-1 kinds
     // run 13-17% faster with 6-plane chunks (tighter lockstep) despite the
     // 2 restart planes per chunk; the others prefer long chunks
-    args.zc = dbg_zc > 0 ? dbg_zc : (Op::R == 1 && Op::NA == 1 && Op::NOUT == 1) ? 6 : 64;
+    // (single-array radius-1 kinds: 6-plane chunks for fp32, 4 for fp64 —
+    // laplacian fp64 512^3 339 -> 377 Gpt/s, jacobi3d fp32 prefers 6)
+    args.zc = dbg_zc > 0 ? dbg_zc : (Op::R == 1 && Op::NA == 1 && Op::NOUT == 1) ? (sizeof(T) == 8 ? 4 : 6) : 64;
     static const int dbg = getenv("STB200_DBG") ? atoi(getenv("STB200_DBG")) : 0;
     args.dbg = dbg;
     // S7 store path (k3d.cuh): the kind's measured choice;

@@ -85,6 +85,7 @@ struct Ctx3 {
 template <typename T> struct OpLap7 {
     static constexpr int R = 1, NA = 1, QA = 0, NOUT = 1, NC = 2;
     static constexpr int STORE = ST_STG;            // S7 store path (measured)
+    static constexpr bool STREAM_ST = true;       // st.global.cs interior stores (measured +2-4%)
     __host__ __device__ static constexpr int box(int) { return BOX_XY; }
     template <class Cx>
     __device__ __forceinline__ static void point(const Cx& x, int p, const Coeffs<T, NC>& c, T* o) {
@@ -101,6 +102,7 @@ template <typename T> struct OpLap7 {
 template <typename T> struct OpWave13 {
     static constexpr int R = 2, NA = 2, QA = 1, NOUT = 1, NC = 3;
     static constexpr int STORE = ST_BULK;           // S7 store path (measured)
+    static constexpr bool STREAM_ST = false;       // st.global.cs interior stores (measured +2-4%)
     __host__ __device__ static constexpr int box(int a) { return a == 0 ? BOX_C : BOX_XY; }  // prev, cur
     template <class Cx>
     __device__ __forceinline__ static void point(const Cx& x, int p, const Coeffs<T, NC>& c, T* o) {
@@ -124,6 +126,7 @@ template <typename T> struct OpWave13 {
 template <typename T> struct OpGradient {
     static constexpr int R = 1, NA = 1, QA = 0, NOUT = 3, NC = 3;
     static constexpr int STORE = ST_STG;            // S7 store path (measured)
+    static constexpr bool STREAM_ST = false;       // st.global.cs interior stores (measured +2-4%)
     __host__ __device__ static constexpr int box(int) { return BOX_XY; }
     template <class Cx>
     __device__ __forceinline__ static void point(const Cx& x, int p, const Coeffs<T, NC>& c, T* o) {
@@ -137,6 +140,7 @@ template <typename T> struct OpGradient {
 template <typename T> struct OpDivergence {
     static constexpr int R = 1, NA = 3, QA = 2, NOUT = 1, NC = 3;
     static constexpr int STORE = ST_STG;            // S7 store path (measured)
+    static constexpr bool STREAM_ST = false;       // st.global.cs interior stores (measured +2-4%)
     __host__ __device__ static constexpr int box(int a) {  // u, v, w
         return a == 0 ? BOX_X : a == 1 ? BOX_Y : BOX_C;
     }
@@ -247,6 +251,14 @@ struct K3Args {
 // a uniform STG.128-only branch (measured slower: DESIGN.md §5.2).
 #ifndef STB200_XIN
 #define STB200_XIN 0
+#endif
+// 1 = SHUFFLE edge fallback as two predicated loads (the first form)
+#ifndef STB200_FB_PRED
+#define STB200_FB_PRED 0
+#endif
+// 1 = interior stores with st.global.cs (evict-first)
+#ifndef STB200_STCS
+#define STB200_STCS 0
 #endif
 
 // ------------------------------------------------------------------ kernel
@@ -381,6 +393,10 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
                             // fallback read of the staged neighbour sector, one
                             // load whose address is lane 0's (x0-R..x0-1) or the
                             // others' (x0+TX..x0+TX+R-1: lane 31's), then selects
+#if STB200_FB_PRED
+                            lds_pred<T, R>(lane0, b + off(a, r, 0, -R), &x.xw[a][0]);
+                            lds_pred<T, R>(lane31, b + off(a, r, 0, V), &x.xw[a][R + V]);
+#else
                             T e[R];
                             {
                                 const T* pe = b + (warp * RY + r + (box_yh(Op::box(a)) ? R : 0)) * L::bx(a) +
@@ -398,6 +414,7 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
                                 x.xw[a][k] = lane0 ? e[k] : x.xw[a][k];
                                 x.xw[a][R + V + k] = lane31 ? e[k] : x.xw[a][R + V + k];
                             }
+#endif
                         } else {                          // PLAIN: neighbours' elements from smem
 #pragma unroll
                             for (int k = 0; k < R; ++k) x.xw[a][k] = b[off(a, r, 0, k - R)];
@@ -427,7 +444,10 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
                     if (STB200_XIN && xin && row_ok) {      // uniform branch: interior warp row
                         stg_vec(op, ov);
                     } else {
-                        if (row_ok && x_vec) stg_vec(op, ov);
+                        if (row_ok && x_vec) {
+                            if (STB200_STCS || Op::STREAM_ST) stcs_vec(op, ov);
+                            else stg_vec(op, ov);
+                        }
 #pragma unroll
                         for (int p = 0; p < V; ++p)
                             if (row_ok && x_el[p]) op[p] = ov[p];
