@@ -47,7 +47,10 @@ WORKLOADS = {
     "wave13pt": dict(kind="wave13pt", dtype="f64", dims=(512, 512, 512), iters=10,
                      config="BASELINE configs[2]: wave13pt 3D 13-point fp64 512^3"),
     "tricubic": dict(kind="tricubic", dtype="f32", dims=(256, 256, 256), iters=10,
-                     config="BASELINE configs[3]: tricubic 3D fp32 256^3"),
+                     config="BASELINE configs[3]: tricubic 3D fp32 256^3",
+                     # FP32 flops per point of the factored form:
+                     # sums 21 mul + 63 fma, weights 9 mul + 15 fma -> 30 + 2*78
+                     flops_per_point=186),
     "jacobi3d": dict(kind="jacobi3d7", dtype="f32", dims=(1024, 1024, 1024), iters=10,
                      config="BASELINE configs[4]: jacobi 3D 7-point fp32 1024^2 x (1024*N)"),
     "divergence": dict(kind="divergence", dtype="f32", dims=(512, 512, 512), iters=10,
@@ -65,6 +68,11 @@ def measured_peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def sm_count():
+    import torch
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
 
 
 def profile_traffic(workload, variant):
@@ -481,6 +489,19 @@ def main():
                                                        (1 if n_bufs == 2 else 0))),
             "cpu_baseline": cpu,
         }
+        if wl.get("flops_per_point"):
+            # the FP32 side of the roofline (the HBM side is the tighter one on
+            # paper: 20 B/pt against 186 flop/pt): nominal 128 FP32 lanes x 2
+            # flop per SM per clock at clocks.max.sm
+            mhz = 1965.0
+            mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+            if os.path.exists(mp):
+                mhz = float(json.load(open(mp)).get("sm_max_mhz", mhz))
+            fpeak = sm_count() * 128 * 2 * mhz * 1e6 / 1e12
+            fach = wl["flops_per_point"] * pts_rank / avg_launch_s / 1e12
+            line["roofline"]["alu"] = {"achieved": fach, "peak": fpeak, "unit": "TFLOP/s", "frac": fach / fpeak,
+                                       "flops_per_point": wl["flops_per_point"],
+                                       "peak_source": "148 SMs x 128 FP32 lanes x 2 flop x clocks.max.sm"}
         print(json.dumps(line), flush=True)
     st.close()
     if world > 1:
