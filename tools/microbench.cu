@@ -141,6 +141,35 @@ __global__ void tput_lds128(int* out, long long* cyc, int iters) {
     if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+// SHFL and LDS.128 interleaved (independent chains): do they share one
+// issue path (MIO)?  ops = 8 SHFL + 8 LDS.128 per thread-iteration; compare
+// the time per iteration with tput_shfl + tput_lds128 (shared) vs their max.
+__global__ void tput_mix(int* out, long long* cyc, int iters) {
+    __shared__ int4 s[2048];
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) s[i] = make_int4(i, i + 1, i + 2, i + 3);
+    __syncthreads();
+    int4 acc = make_int4(0, 0, 0, 0);
+    int v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = threadIdx.x + k;
+    int idx = threadIdx.x & 31;
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            v[k] = __shfl_up_sync(0xffffffffu, v[k], 1);
+            int4 t = s[(idx + 32 * k + i) & 2047];
+            acc.x ^= t.x; acc.y ^= t.y; acc.z ^= t.z; acc.w ^= t.w;
+        }
+    }
+    long long t1 = clock64();
+    int r = acc.x + acc.y + acc.z + acc.w;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r += v[k];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = r;
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 static int nsm() {
     int n;
     CK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, 0));
@@ -199,6 +228,8 @@ int main() {
     printf("\"ffma_imm\": %.1f, ", per_sm_rate([&](long long* c) { tput_fma<2><<<nb, nt>>>((float*)dout, c, 1.0001f, it); }, nb, nt, it, 8));
     printf("\"ffma2_fma_lanes\": %.1f, ", per_sm_rate([&](long long* c) { tput_ffma2<<<nb, nt>>>((float*)dout, c, 1.0001f, it); }, nb, nt, it, 16));
     printf("\"shfl_lanes\": %.1f, ", per_sm_rate([&](long long* c) { tput_shfl<<<nb, nt>>>(dout, c, it); }, nb, nt, it, 8));
-    printf("\"lds128_lanes\": %.1f}}\n", per_sm_rate([&](long long* c) { tput_lds128<<<nb, nt>>>(dout, c, it); }, nb, nt, it, 8));
+    printf("\"lds128_lanes\": %.1f, ", per_sm_rate([&](long long* c) { tput_lds128<<<nb, nt>>>(dout, c, it); }, nb, nt, it, 8));
+    // iterations of (1 SHFL + 1 LDS.128) per SM per clock, in lanes
+    printf("\"shfl_plus_lds128_pair_lanes\": %.1f}}\n", per_sm_rate([&](long long* c) { tput_mix<<<nb, nt>>>(dout, c, it); }, nb, nt, it, 8));
     return 0;
 }
