@@ -152,6 +152,14 @@ template <typename T> struct OpDivergence {
     }
 };
 
+// deepest plane ring (stages) a kind may use, shared memory permitting
+#ifndef STB200_NSMAX
+#define STB200_NSMAX 8
+#endif
+#ifndef STB200_SMEM_KB
+#define STB200_SMEM_KB 200
+#endif
+
 // ----------------------------------------------------------- smem layout
 // CTA tile: TX = 32*V columns by TY = kWarps3D*RY = 30 rows; each consumer
 // warp owns RY = 2 consecutive rows (its z queues fit the register budget of
@@ -188,8 +196,8 @@ struct Layout3 {
         return Op::STORE == ST_BULK ? kWarps3D * RY * Op::NOUT * OUT_ROW : 0;
     }
     // stages: as many as fit in ~200 KB with the staging (one CTA per SM), at least 2R+2
-    static constexpr int NS_FIT = (200 * 1024 - out_bytes()) / stage_bytes();
-    static constexpr int NS = NS_FIT > 8 ? 8 : (NS_FIT < 2 * R + 2 ? 2 * R + 2 : NS_FIT);
+    static constexpr int NS_FIT = (STB200_SMEM_KB * 1024 - out_bytes()) / stage_bytes();
+    static constexpr int NS = NS_FIT > STB200_NSMAX ? STB200_NSMAX : (NS_FIT < 2 * R + 2 ? 2 * R + 2 : NS_FIT);
     static constexpr size_t out_off() { return (size_t)NS * stage_bytes(); }
     static constexpr size_t smem_bytes() {
         return out_off() + out_bytes() + 2 * NS * sizeof(uint64_t);
