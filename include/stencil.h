@@ -75,8 +75,9 @@ enum stencil_dtype { ST_F32 = 1, ST_F64 = 2, ST_I32 = 3 };
  *              PAPER.md:561-564).
  *  ST_PLAIN:   the same taps come from loads (L1 / shared memory), i.e. the
  *              original code's loads, no shuffles.
- * The paper-literal family (2-D kinds, fp32/int32 only: the paper shuffles
- * 32-bit data): one output per thread, 512 threads per
+ * The paper-literal family (every kind in fp32/int32 only: the paper
+ * shuffles 32-bit data; not with the fused peer-store
+ * transport, ST_EUNSUPPORTED): one output per thread, 512 threads per
  * block along x (Listing 5), leftmost tap of each x-row as
  * the shuffle source, written as the PTX of Listing 6:
  *  ST_PAPER_ORIGINAL: every tap an ld.global.nc (the compiler's code)

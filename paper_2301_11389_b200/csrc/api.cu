@@ -126,10 +126,14 @@ extern "C" int stencil_set_variant(stencil_t h, int variant) {
     if (!h) return set_error(ST_EARG, "null handle");
     if (variant < ST_SHUFFLE || variant > ST_PAPER_UNIFORM)
         return set_error(ST_EUNSUPPORTED, "unknown variant %d", variant);
-    if (variant >= ST_PAPER_ORIGINAL && (h->ndims != 2 || h->dtype == ST_F64))
+    if (variant >= ST_PAPER_ORIGINAL && h->dtype == ST_F64)
         return set_error(ST_EUNSUPPORTED,
-                         "the paper-literal variants cover the 2-D fp32/int32 kinds (32-bit shuffles, "
+                         "the paper-literal variants cover the fp32/int32 kinds (32-bit shuffles, "
                          "PAPER.md:272-274)");
+    if (variant >= ST_PAPER_ORIGINAL && dist_is_p2p(h))
+        return set_error(ST_EUNSUPPORTED,
+                         "the paper-literal variants have no fused peer-store epilogue: use the NCCL or "
+                         "host transport");
     h->variant = variant;
     return ST_OK;
 }

@@ -10,6 +10,7 @@
 #include "k3d.cuh"
 #include "ktricubic.cuh"
 #include "ktricubic2.cuh"
+#include "kpaper3d.cuh"
 
 namespace stb200 {
 
@@ -132,9 +133,58 @@ static cudaError_t launch3_var(const stencil_s* h, const void* const* in, void* 
 cudaError_t launch_tricubic(const stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
                             int64_t z_lo, int64_t z_hi);
 
+// The paper-literal family for the 3-D kinds (kpaper3d.cuh): one output per
+// thread, 512 threads per block along x, one block per (x block, row, plane).
+template <int KIND, int PV>
+static cudaError_t launch_kpaper3d(const stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
+                                   int64_t z_lo, int64_t z_hi) {
+    const int64_t* ld = h->ldims;
+    const int lo = h->k->lo, hi = h->k->hi;
+    if (z_lo < 0) { z_lo = lo; z_hi = ld[2] - hi; }
+    if (z_hi <= z_lo) return cudaSuccess;
+    const int64_t rows = ld[1] - lo - hi;
+    if (rows > 65535 || z_hi - z_lo > 65535) return cudaErrorInvalidConfiguration;
+    P3Args a{};
+    for (int t = 0; t < h->k->n_in; ++t) a.in[t] = (const uint32_t*)in[t];
+    for (int t = 0; t < h->k->n_out; ++t) a.out[t] = (float*)out[t];
+    a.nx = ld[0];
+    a.ny = ld[1];
+    a.z_lo = (int)z_lo;
+    a.lo = lo;
+    a.hi = hi;
+    for (int t = 0; t < 3 && t < h->k->ncoeffs; ++t) a.c[t] = (float)h->coeffs[t];
+    const dim3 grid((unsigned)((ld[0] - lo - hi + kPaperThreads - 1) / kPaperThreads), (unsigned)rows,
+                    (unsigned)(z_hi - z_lo));
+    kpaper3d<KIND, PV><<<grid, kPaperThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int KIND>
+static cudaError_t paper3_var(const stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
+                              int64_t a, int64_t b) {
+    switch (h->variant) {
+    case ST_PAPER_ORIGINAL: return launch_kpaper3d<KIND, PV_ORIGINAL>(h, in, out, s, a, b);
+    case ST_PAPER_PTXASW: return launch_kpaper3d<KIND, PV_PTXASW>(h, in, out, s, a, b);
+    case ST_PAPER_NOLOAD: return launch_kpaper3d<KIND, PV_NOLOAD>(h, in, out, s, a, b);
+    case ST_PAPER_NOCORNER: return launch_kpaper3d<KIND, PV_NOCORNER>(h, in, out, s, a, b);
+    default: return launch_kpaper3d<KIND, PV_UNIFORM>(h, in, out, s, a, b);
+    }
+}
+
 cudaError_t dispatch_3d(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
                         int64_t a, int64_t b) {
     const bool f64 = h->dtype == ST_F64;
+    if (h->variant >= ST_PAPER_ORIGINAL) {                 // validated fp32 in set_variant
+        switch (h->k->kind) {
+        case ST_LAPLACIAN3D7:
+        case ST_JACOBI3D7: return paper3_var<1>(h, in, out, s, a, b);
+        case ST_WAVE13PT: return paper3_var<2>(h, in, out, s, a, b);
+        case ST_DIVERGENCE: return paper3_var<3>(h, in, out, s, a, b);
+        case ST_GRADIENT: return paper3_var<4>(h, in, out, s, a, b);
+        case ST_TRICUBIC: return paper3_var<5>(h, in, out, s, a, b);
+        default: return cudaErrorInvalidValue;
+        }
+    }
     switch (h->k->kind) {
     case ST_LAPLACIAN3D7:
     case ST_JACOBI3D7:

@@ -265,6 +265,8 @@ constexpr uint32_t kBlobMagic = 0x53503250u;   // "P2PS"
 }
 
 extern "C" int stencil_dist_attach_p2p(stencil_t h, int rank, int nranks) {
+    if (h && h->variant >= ST_PAPER_ORIGINAL)
+        return set_error(ST_EUNSUPPORTED, "paper-literal variants cannot use the fused peer-store transport");
     if (!drv().ok) return set_error(ST_EUNSUPPORTED, "driver stream memory operations unavailable");
     DistState* d = nullptr;
     int rc = dist_attach_common(h, rank, nranks, &d);

@@ -24,31 +24,53 @@ VARIANTS = ["paper_original", "paper_ptxasw", "paper_noload", "paper_nocorner", 
             "plain", "shuffle"]
 
 
-def time_variant(kind, dtype, n, runs, var, a, b):
-    st = Stencil(kind, (n, n), dtype, variant=var)
+def time_variant(kind, dtype, dims, runs, var, ins, outs):
+    st = Stencil(kind, dims, dtype, variant=var)
     for _ in range(3):
-        st.step([a], [b])
+        st.step(ins, outs)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(runs):
-        st.step([a], [b])
+        st.step(ins, outs)
     e1.record()
     torch.cuda.synchronize()
     st.close()
     return e0.elapsed_time(e1)
 
 
+# 3-D suite members: (kind, inputs, outputs, lo, hi)
+KINDS_3D = [("laplacian3d7", 1, 1, 1, 1), ("wave13pt", 2, 1, 2, 2), ("divergence", 3, 1, 1, 1),
+            ("gradient", 1, 3, 1, 1), ("tricubic", 4, 1, 1, 2)]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=32768)
     ap.add_argument("--runs", type=int, default=10)
+    ap.add_argument("--dims3", default="512,1024,1024",
+                    help="3-D grid nx,ny,nz (the paper's 512x1024x1024, PAPER.md:645)")
+    ap.add_argument("--no-2d", action="store_true")
     args = ap.parse_args()
-    out = {"source": "tools/paper_fig3.py", "grid": [args.n, args.n], "runs": args.runs, "results": {}}
-    for kind, dtype in (("jacobi2d9", "f32"), ("gaussblur5x5", "f32"), ("gameoflife", "i32")):
+    d3 = tuple(int(x) for x in args.dims3.split(","))
+    out = {"source": "tools/paper_fig3.py", "grid": [args.n, args.n], "grid3": list(d3), "runs": args.runs,
+           "results": {}}
+    for kind, nin, nout, lo, hi in KINDS_3D:
+        shape = d3[::-1]
+        ins = [inputs.generate_torch(shape, "f32", inputs.BASE_SEED + 31, a) for a in range(nin)]
+        outs = [torch.zeros_like(ins[0]) for _ in range(nout)]
+        ms = {v: time_variant(kind, "f32", d3, args.runs, v, ins, outs) for v in VARIANTS}
+        pts = (d3[0] - lo - hi) * (d3[1] - lo - hi) * (d3[2] - lo - hi) * args.runs
+        out["results"][kind] = {
+            v: {"ms": ms[v], "gpts": pts / (ms[v] / 1e3) / 1e9,
+                "speedup_vs_original": ms["paper_original"] / ms[v]} for v in VARIANTS}
+        del ins, outs
+        torch.cuda.empty_cache()
+    for kind, dtype in (() if args.no_2d else (("jacobi2d9", "f32"), ("gaussblur5x5", "f32"),
+                                                ("gameoflife", "i32"))):
         a = inputs.generate_torch((args.n, args.n), dtype, inputs.BASE_SEED + 30)
         b = torch.zeros_like(a)
-        ms = {v: time_variant(kind, dtype, args.n, args.runs, v, a, b) for v in VARIANTS}
+        ms = {v: time_variant(kind, dtype, (args.n, args.n), args.runs, v, [a], [b]) for v in VARIANTS}
         pts = (args.n - 2 * (2 if kind == "gaussblur5x5" else 1)) ** 2 * args.runs
         out["results"][kind] = {
             v: {"ms": ms[v], "gpts": pts / (ms[v] / 1e3) / 1e9,
