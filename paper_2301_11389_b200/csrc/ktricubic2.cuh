@@ -34,16 +34,26 @@ namespace stb200 {
 
 constexpr int kTri2Warps = 11;    // consumer warps (+1 producer = 12 warps: 3 per SMSP, <=168 regs), 2 rows each
 
+#ifndef STB200_TRI2_NS
+#define STB200_TRI2_NS 8          // f plane ring stages
+#endif
+#ifndef STB200_TRI2_NO
+#define STB200_TRI2_NO 3          // X/Y/Z offset ring stages
+#endif
+#ifndef STB200_TRI2_LAG
+#define STB200_TRI2_LAG 2         // offsets of output plane o are issued after f plane o + LAG
+#endif
+
 struct Tri2Layout {
     static constexpr int V = 4, TX = 128, RY = 2, TY = kTri2Warps * RY, PADX = 8;
     static constexpr int FBX = TX + 2 * PADX, FBY = TY + 3;       // f box: x0-8 .. x0+135, rows y0-1 .. y0+TY+1
     static constexpr int F_BYTES = FBX * FBY * 4;
     static constexpr int STAGE = (F_BYTES + 127) / 128 * 128;
-    static constexpr int NS = 8;                                 // 4 planes in use + 4 in flight
+    static constexpr int NS = STB200_TRI2_NS;                    // 4 planes in use + 4 in flight
     // offsets X, Y, Z of one output plane: three (TX x TY) boxes per stage
     static constexpr int O_BYTES = TX * TY * 4;
     static constexpr int OSTAGE = 3 * O_BYTES;
-    static constexpr int NO = 3;
+    static constexpr int NO = STB200_TRI2_NO;
     static constexpr size_t SMEM = (size_t)NS * STAGE + (size_t)NO * OSTAGE + 2 * (NS + NO) * sizeof(uint64_t);
 };
 
@@ -86,6 +96,10 @@ __device__ __forceinline__ float phi(pr v) {
     asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
     return b;
 }
+#ifndef STB200_TRI2_SCALAR
+#define STB200_TRI2_SCALAR 0      // experiment: every pair op as two scalar FFMA/FMUL
+#endif
+#if !STB200_TRI2_SCALAR
 __device__ __forceinline__ pr fma2(pr a, pr b, pr c) {
     pr d;
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
@@ -99,6 +113,14 @@ __device__ __forceinline__ pr mul2(pr a, pr b) {
 // a * {f, f} (+ c): the tap f is a broadcast operand
 __device__ __forceinline__ pr fma2s(pr a, float f, pr c) { return fma2(a, pk(f, f), c); }
 __device__ __forceinline__ pr mul2s(pr a, float f) { return mul2(a, pk(f, f)); }
+#else
+__device__ __forceinline__ pr fma2(pr a, pr b, pr c) {
+    return pk(fmaf(plo(a), plo(b), plo(c)), fmaf(phi(a), phi(b), phi(c)));
+}
+__device__ __forceinline__ pr mul2(pr a, pr b) { return pk(plo(a) * plo(b), phi(a) * phi(b)); }
+__device__ __forceinline__ pr fma2s(pr a, float f, pr c) { return pk(fmaf(plo(a), f, plo(c)), fmaf(phi(a), f, phi(c))); }
+__device__ __forceinline__ pr mul2s(pr a, float f) { return pk(plo(a) * f, phi(a) * f); }
+#endif
 __device__ __forceinline__ pr cst(float v) { return pk(v, v); }
 __device__ __forceinline__ void ldsv(float* v, const float* p) {
     const float4 t = *reinterpret_cast<const float4*>(p);
@@ -170,8 +192,8 @@ ktricubic2(const __grid_constant__ TmapPack<4> tm, const __grid_constant__ TriAr
                     mbar_arrive_expect_tx(&full[s], L::F_BYTES);
                     tma_load_3d(smem + (size_t)s * L::STAGE, &tm.m[0], tx * TX - PADX, ty * TY - 1,
                                 z_first + t, &full[s]);
-                    // offsets of output plane t-2 after f plane t (two planes of lead)
-                    const int o = t - 2;
+                    // offsets of output plane t-LAG after f plane t
+                    const int o = t - STB200_TRI2_LAG;
                     if (o >= 0 && o < nseg) {
                         const uint32_t so = go % NO;
                         if (go >= NO) mbar_wait_backoff<1024>(&oempty[so], (go / NO - 1) & 1u);
