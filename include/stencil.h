@@ -117,16 +117,24 @@ int stencil_set_variant(stencil_t h, int variant);
 int stencil_get_variant(stencil_t h, int* variant);
 
 /* Temporal blocking of 2-D ping-pong runs: stencil_run may
- * apply several sweeps per kernel launch, each CTA sweeping its tile plus an
- * S*R halo in shared memory; results are bit-identical to single sweeps.
- *   0 (default) auto: fused for L2-resident grids (<= 8 MiB per buffer),
- *                     where per-launch latency bounds the run
- *   1           never fuse
- *   S >= 2      at most S sweeps per launch (capped by shared memory)
+ * apply several sweeps per kernel launch; results are bit-identical to
+ * single sweeps.
+ *   0 (default) auto: grids that sit in L2 (<= 8 MiB per buffer) run the
+ *                     shared-memory tile kernel (each CTA sweeps its tile plus
+ *                     an S*R halo, S as deep as shared memory allows: per-
+ *                     launch latency bounds those runs); larger jacobi2d5 /
+ *                     jacobi2d9 grids run the streaming two-sweep
+ *                     register-cache kernel (one HBM pass per two sweeps:
+ *                     the single-sweep kernel is HBM-bound); gaussblur and
+ *                     gameoflife keep one sweep per launch (issue-bound at
+ *                     two sweeps per pass)
+ *   1           never fuse (one sweep per launch)
+ *   2           the streaming two-sweep kernel, any grid size
+ *   S >= 3      the tile kernel with at most S sweeps per launch
  * Only the register-cache variants (SHUFFLE/PLAIN) and single-GPU handles
- * fuse; stencil_step is always one sweep.  A fused run leaves the result in
- * bufs[n_iters % 2] like single sweeps; the other buffer holds an earlier
- * sweep. */
+ * fuse; stencil_step is always one sweep.  The result buffer of a run is
+ * reported in *result_idx (fused runs may differ from n_iters % 2); the
+ * other buffer holds an earlier sweep. */
 int stencil_set_fusion(stencil_t h, int sweeps_per_launch);
 
 /* Arity: inputs and outputs of one step; buffers stencil_run expects
@@ -142,6 +150,8 @@ typedef struct {
     int64_t interior_points;  /* points one step writes on this rank                */
     double bytes_per_point;   /* compulsory HBM bytes per interior point per step   */
     int launches_per_step;    /* kernels one stencil_step enqueues                  */
+    int sweeps_per_launch;    /* sweeps per sweep-kernel launch of a long stencil_run
+                                 on this handle (1, 2 = streaming pair, S = tile)   */
     int rank, nranks;         /* 0,1 unless attached                                */
 } stencil_info_t;
 int stencil_info(stencil_t h, stencil_info_t* out);

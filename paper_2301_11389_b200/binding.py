@@ -47,7 +47,8 @@ class stencil_info_t(ctypes.Structure):
                 ("variant", ctypes.c_int), ("dims", ctypes.c_int64 * 3),
                 ("local_dims", ctypes.c_int64 * 3), ("lo", ctypes.c_int), ("hi", ctypes.c_int),
                 ("interior_points", ctypes.c_int64), ("bytes_per_point", ctypes.c_double),
-                ("launches_per_step", ctypes.c_int), ("rank", ctypes.c_int),
+                ("launches_per_step", ctypes.c_int), ("sweeps_per_launch", ctypes.c_int),
+                ("rank", ctypes.c_int),
                 ("nranks", ctypes.c_int)]
 
 

@@ -189,6 +189,7 @@ extern "C" int stencil_info(stencil_t h, stencil_info_t* o) {
     int reads = h->k->n_in, writes = h->k->n_out;
     o->bytes_per_point = (double)(reads + writes) * (double)dtype_size(h->dtype);
     o->launches_per_step = h->dist ? dist_launches_per_step(h) : 1;
+    o->sweeps_per_launch = sweeps_per_launch(h, 100);
     o->rank = h->dist ? h->rank : 0;
     o->nranks = h->dist ? h->nranks : 1;
     return ST_OK;
@@ -317,13 +318,36 @@ int stb200::ring_copy(const stencil_s* h, const void* src, void* dst, cudaStream
 // Sweeps per launch of a 2-D ping-pong run: the handle's fusion setting, or
 // (auto) fused when the grid is L2-resident (<= 8 MiB per buffer) and the
 // run has several sweeps: there per-launch latency, not HBM, bounds it.
-static int fusion_depth(const stencil_s* h, int n_iters) {
-    if (h->ndims != 2 || h->dist || h->k->iterable != 1 || n_iters < 2 || h->variant > ST_PLAIN) return 1;
-    const int smax = fused_max_sweeps(h);
-    if (h->fusion >= 2) return h->fusion < smax ? h->fusion : smax;
-    if (h->fusion == 1) return 1;
+static bool fusable(const stencil_s* h) {
+    return h->ndims == 2 && !h->dist && h->k->iterable == 1 && h->variant <= ST_PLAIN;
+}
+static bool l2_resident(const stencil_s* h) {
     const size_t bytes = (size_t)h->ldims[0] * h->ldims[1] * (h->dtype == ST_F64 ? 8 : 4);
-    return bytes <= ((size_t)8 << 20) ? smax : 1;
+    return bytes <= ((size_t)8 << 20);
+}
+// Sweeps per launch of the shared-memory tile kernel (ktb2d) for a run, or 1.
+static int fusion_depth(const stencil_s* h, int n_iters) {
+    if (!fusable(h) || n_iters < 2) return 1;
+    const int smax = fused_max_sweeps(h);
+    if (h->fusion >= 3) return h->fusion < smax ? h->fusion : smax;
+    if (h->fusion == 0 && l2_resident(h)) return smax;
+    return 1;
+}
+// Two sweeps per launch through the streaming kernel (k2d2): forced with
+// fusion == 2; automatic for the Jacobi kinds on grids that do not sit in L2.
+// Measured on B200: jacobi2d5 32768^2 fp32 846 -> 1217-1268
+// Gpt/s, jacobi2d9 845 -> 1040, fp64 16384^2 +55-71%; gaussblur (25 FMA/pt)
+// and gameoflife are issue-bound at two sweeps per pass and run slower, so
+// they keep one sweep per launch.
+static bool pair_fusion(const stencil_s* h, int n_iters) {
+    if (!fusable(h) || n_iters < 2) return false;
+    if (h->fusion == 2) return true;
+    const bool cheap = h->k->kind == ST_JACOBI2D5 || h->k->kind == ST_JACOBI2D9;
+    return h->fusion == 0 && cheap && !l2_resident(h);
+}
+int stb200::sweeps_per_launch(const stencil_s* h, int n_iters) {
+    if (pair_fusion(h, n_iters)) return 2;
+    return fusion_depth(h, n_iters);
 }
 
 static int enqueue_run(stencil_s* h, void* const* bufs, int n_iters, cudaStream_t s, int* result) {
@@ -331,6 +355,27 @@ static int enqueue_run(stencil_s* h, void* const* bufs, int n_iters, cudaStream_
     int rc;
     if (dist_is_p2p(h)) return p2p_run(h, bufs, n_iters, s, result);
     if (k->iterable == 1) {
+        if (pair_fusion(h, n_iters)) {
+            // two sweeps per launch (k2d2); an odd count starts with one
+            // single sweep.  The ring stays fixed: copy it once, as below.
+            if ((rc = ring_copy(h, bufs[0], bufs[1], s))) return rc;
+            int cur = 0, done = 0;
+            if (n_iters & 1) {
+                const void* in[1] = {bufs[0]};
+                void* out[1] = {bufs[1]};
+                if ((rc = launch_sweep(h, in, out, s, -1, -1))) return rc;
+                cur = 1;
+                done = 1;
+            }
+            for (; done < n_iters; done += 2) {
+                cudaError_t e = dispatch_2d_pair(h, bufs[cur], bufs[1 - cur], s);
+                if (e != cudaSuccess)
+                    return set_error(ST_ECUDA, "%s two-sweep launch failed: %s", k->name, cudaGetErrorString(e));
+                cur = 1 - cur;
+            }
+            *result = cur;
+            return ST_OK;
+        }
         const int S = fusion_depth(h, n_iters);
         if (S > 1) {
             // passes of <= S sweeps (the fused kernel also writes the ring

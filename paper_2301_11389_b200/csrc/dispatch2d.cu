@@ -5,6 +5,7 @@
 #include "k2d.cuh"
 #include "kpaper.cuh"
 #include "ktb2d.cuh"
+#include "k2d2.cuh"
 
 namespace stb200 {
 
@@ -155,6 +156,56 @@ static cudaError_t launch_tb(const stencil_s* h, const void* in, void* out, cuda
     for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)h->coeffs[t];
     ktb2d<Op, T><<<grid, kTbThreads, smem, s>>>((const T*)in, (T*)out, (int)nx, (int)ny, S, c);
     return cudaGetLastError();
+}
+
+// Two sweeps per launch, streaming (k2d2.cuh): the large-grid form of
+// temporal blocking.  Strips of H sweep-2 rows in blockIdx order, as k2d.
+template <class Op, typename T, int VAR>
+static cudaError_t launch_k2d2(const stencil_s* h, const void* in, void* out, cudaStream_t s) {
+    constexpr int R = Op::R;
+    constexpr int kStripH = 24;
+    auto kern = k2d2<Op, T, VAR>;
+    constexpr size_t smem = k2d2_smem_bytes<T>();
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const int64_t nx = h->ldims[0], ny = h->ldims[1];
+    const int64_t y_lo = R, y_hi = ny - R;
+    if (y_hi <= y_lo) return cudaSuccess;
+    const int64_t gx = (nx + kWarps2D * k2d2_txo<T>() - 1) / (kWarps2D * k2d2_txo<T>());
+    const int64_t rows = y_hi - y_lo;
+    static const int dbg_h = getenv("STB200_2D2_H") ? atoi(getenv("STB200_2D2_H")) : 0;
+    int64_t H = (rows * gx + 2 * sm_count(h->device) - 1) / (2 * sm_count(h->device));
+    H = H < 4 ? 4 : H > kStripH ? kStripH : H;
+    if (dbg_h > 0) H = dbg_h;
+    const int64_t nstrips = (rows + H - 1) / H;
+    if (nstrips > 65535 || ny > INT32_MAX) return cudaErrorInvalidConfiguration;
+    Coeffs<T, Op::NC> c{};
+    for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)h->coeffs[t];
+    kern<<<dim3((unsigned)gx, (unsigned)nstrips), k2d_threads(), smem, s>>>(
+        (const T*)in, (T*)out, nx, (int)ny, (int)y_lo, (int)y_hi, (int)H, c);
+    return cudaGetLastError();
+}
+
+template <template <typename> class OpT, typename T>
+static cudaError_t pair_var(const stencil_s* h, const void* in, void* out, cudaStream_t s) {
+    if (h->variant == ST_PLAIN) return launch_k2d2<OpT<T>, T, VAR_PLAIN>(h, in, out, s);
+    return launch_k2d2<OpT<T>, T, VAR_SHUFFLE>(h, in, out, s);
+}
+
+cudaError_t dispatch_2d_pair(stencil_s* h, const void* in, void* out, cudaStream_t s) {
+    const bool f64 = h->dtype == ST_F64;
+    switch (h->k->kind) {
+    case ST_JACOBI2D5: return f64 ? pair_var<OpJacobi2D5, double>(h, in, out, s) : pair_var<OpJacobi2D5, float>(h, in, out, s);
+    case ST_JACOBI2D9: return f64 ? pair_var<OpJacobi2D9, double>(h, in, out, s) : pair_var<OpJacobi2D9, float>(h, in, out, s);
+    case ST_GAUSSBLUR5X5: return f64 ? pair_var<OpGauss5, double>(h, in, out, s) : pair_var<OpGauss5, float>(h, in, out, s);
+    case ST_GAMEOFLIFE:
+        if (h->variant == ST_PLAIN) return launch_k2d2<OpLife, int, VAR_PLAIN>(h, in, out, s);
+        return launch_k2d2<OpLife, int, VAR_SHUFFLE>(h, in, out, s);
+    default: return cudaErrorInvalidValue;
+    }
 }
 
 // Largest fusion depth whose two shared-memory planes fit in ~100 KB.

@@ -1,0 +1,228 @@
+// k2d2.cuh — two sweeps per HBM pass for the large 2-D ping-pong runs
+// ("multiple sweeps per HBM pass"), register-cache
+// form of k2d.cuh.
+//
+// A single sweep of the 2-D kinds is HBM-bound at ~8 B/pt (k2d runs at
+// 0.96-1.04 of the copy peak), so the only way past that roofline is to
+// read and write each element once per TWO sweeps.  Per warp, per staged
+// input row:
+//
+//   input row -> register window (as k2d: LDS.128 + x halo)
+//            -> sweep-1 row (Op::point, the same arithmetic as k2d; cells
+//               on the grid's boundary ring keep their input value — the
+//               Dirichlet ring stencil_run holds fixed)
+//            -> sweep-1 register window (x halo of the sweep-1 row from the
+//               neighbour lanes: shfl.up/down for SHUFFLE, a per-warp staged
+//               row in shared memory for PLAIN)
+//            -> sweep-2 row (Op::point again) -> STG.128.
+//
+// Overlapped warp tiles: a warp computes sweep 1 on its 32 lanes x V
+// columns; lanes 0 and 31 lack one side of the sweep-1 halo, so sweep-2
+// results are stored by lanes 1..30 only (30 V columns per warp, 120 fp32).
+// Adjacent warps' tiles overlap by 2 V columns (6.7% redundant sweep-1
+// work).  A strip of H sweep-2 rows reads H + 4R input rows (the 2R extra
+// rows on each side are shared with the neighbouring strips through L2).
+// Results are bit-identical to two separate k2d sweeps.
+#pragma once
+#include "k2d.cuh"
+
+namespace stb200 {
+
+template <typename T> constexpr int k2d2_txo() { return 30 * vlen<T>(); }       // sweep-2 columns per warp
+template <typename T> constexpr int k2d2_row_elems() { return kWarps2D * k2d2_txo<T>() + 4 * vlen<T>(); }
+template <typename T>
+constexpr size_t k2d2_smem_bytes() {
+    return (size_t)kStages2D * (k2d2_row_elems<T>() * sizeof(T) + 2 * sizeof(uint64_t)) +
+           (size_t)kWarps2D * (32 + 2) * vlen<T>() * sizeof(T);        // PLAIN: per-warp sweep-1 row
+}
+
+// Grid: x = ceil(nx / (kWarps2D * 30V)), y = strips of H sweep-2 rows
+// covering [y_lo, y_hi) (R <= y_lo, y_hi <= ny - R).
+template <class Op, typename T, int VARIANT>
+__global__ void __launch_bounds__(k2d_threads())
+k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo, int y_hi, int H,
+     Coeffs<T, Op::NC> c) {
+    constexpr int R = Op::R;
+    constexpr int V = vlen<T>();
+    constexpr int TXO = k2d2_txo<T>();
+    constexpr int W = V + 2 * R;
+    constexpr int NW = 2 * R + 1;
+    constexpr int WS = k2d2_row_elems<T>();
+    constexpr int S = kStages2D;
+    static_assert(R <= V, "halo wider than the staging pad");
+    constexpr unsigned LOG2S = S == 2 ? 1 : S == 4 ? 2 : S == 8 ? 3 : S == 16 ? 4 : 5;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* ring = reinterpret_cast<T*>(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * WS * sizeof(T));
+    uint64_t* empty = full + S;
+    T* s1row = reinterpret_cast<T*>(empty + S);            // PLAIN: [kWarps2D][32V + 2V]
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = lane_id();
+    const int64_t X0 = (int64_t)blockIdx.x * (kWarps2D * TXO);       // CTA's first sweep-2 column
+    const int ys = y_lo + (int)blockIdx.y * H;
+    const int ye = min(ys + H, y_hi);
+    if (ys >= ye) return;                                  // CTA-uniform
+    const int row0 = ys - 2 * R;                           // first input row of the strip
+    const int nrows = ye - ys + 4 * R;                     // input rows [ys-2R, ye+2R)
+    const int64_t n_left = (nx - X0 + TXO - 1) / TXO;
+    const int active = n_left < kWarps2D ? (int)n_left : kWarps2D;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], active * 32);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    if (warp == kWarps2D) {                                // ---- producer warp
+        if (lane == 0) {
+            // staged element e <-> global column X0 - 2V + e; clip to [0, nx)
+            const int64_t g_lo = X0 - 2 * V > 0 ? X0 - 2 * V : 0;
+            const int64_t g_hi0 = X0 + kWarps2D * TXO + 2 * V;
+            const int64_t g_hi = g_hi0 < nx ? g_hi0 : nx;
+            const uint32_t bytes = (uint32_t)((g_hi - g_lo) * (int64_t)sizeof(T));
+            T* dst0 = ring + (g_lo - (X0 - 2 * V));
+            for (int r = 0; r < nrows; ++r) {
+                const unsigned s = (unsigned)r & (S - 1);
+                if (r >= S) mbar_wait_backoff<256>(&empty[s], (((unsigned)r >> LOG2S) - 1) & 1u);
+                const int yin = row0 + r;
+                if (yin >= 0 && yin < ny) {
+                    mbar_arrive_expect_tx(&full[s], bytes);
+                    bulk_g2s(dst0 + s * WS, in + (int64_t)yin * nx + g_lo, bytes, &full[s]);
+                } else {
+                    mbar_arrive(&full[s]);                 // outside the grid: never used
+                }
+            }
+        }
+        return;
+    }
+    if (warp >= active) return;                            // past the row end
+
+    // ---- consumer warps
+    const int64_t xs = X0 + (int64_t)warp * TXO - V;       // sweep-1 column of lane 0
+    const int64_t xl = xs + lane * V;                      // first column of this lane
+    const int lo_e = warp * TXO + V + lane * V;            // staged element of column xl
+    const bool lane0 = lane == 0, lane31 = lane == 31;
+    T win[NW][W];                                          // input rows
+    T w1[NW][W];                                           // sweep-1 rows
+
+    auto consume = [&](unsigned r, T* dst) {
+        const unsigned s = r & (S - 1);
+        mbar_wait(&full[s], (r >> LOG2S) & 1u);
+        const T* row = ring + s * WS;
+        T v[V];
+        {
+            using VT = typename VecOf<T>::type;
+            const VT t = *reinterpret_cast<const VT*>(row + lo_e);
+            if constexpr (V == 4) { v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w; }
+            else { v[0] = t.x; v[1] = t.y; }
+        }
+#pragma unroll
+        for (int k = 0; k < V; ++k) dst[R + k] = v[k];
+        if constexpr (VARIANT == VAR_SHUFFLE) {
+#pragma unroll
+            for (int k = 0; k < R; ++k) dst[k] = shfl_up(v[V - R + k], 1);
+#pragma unroll
+            for (int k = 0; k < R; ++k) dst[R + V + k] = shfl_down(v[k], 1);
+            lds_pred<T, R>(lane0, row + lo_e - R, dst);     // warp-edge fallback
+            lds_pred<T, R>(lane31, row + lo_e + V, dst + R + V);
+        } else {
+#pragma unroll
+            for (int k = 0; k < R; ++k) dst[k] = row[lo_e - R + k];
+#pragma unroll
+            for (int k = 0; k < R; ++k) dst[R + V + k] = row[lo_e + V + k];
+        }
+        mbar_arrive(&empty[s]);
+    };
+
+    // per-element masks: interior columns (sweep 1 computes, else keeps the
+    // input value) and the sweep-2 stores (lanes 1..30, interior only)
+    bool xin[V];
+#pragma unroll
+    for (int p = 0; p < V; ++p) xin[p] = xl + p >= R && xl + p < nx - R;
+    const bool own = xl < nx && lane >= 1 && lane <= 30;
+    const bool vec_store = own && xl >= R && xl + V <= nx - R;
+    bool el_store[V];
+#pragma unroll
+    for (int p = 0; p < V; ++p) el_store[p] = !vec_store && own && xin[p];
+    Coeffs<T, Op::NC> cr;
+#pragma unroll
+    for (int t = 0; t < Op::NC; ++t) cr.c[t] = c.c[t];
+    T* srow = s1row + warp * (32 + 2) * V + V;             // PLAIN staging: element e <-> column xs + e
+
+    auto point_row = [&](const auto& w, T* o) {
+        if constexpr (HasPaired<Op>::value) {
+#pragma unroll
+            for (int p = 0; p < V; p += 2) {
+                const float2 r = Op::point2(w, p, cr);
+                o[p] = r.x;
+                o[p + 1] = r.y;
+            }
+        } else {
+#pragma unroll
+            for (int p = 0; p < V; ++p) o[p] = Op::point(w, p, cr);
+        }
+    };
+
+    // one staged input row: t = sweep-1 row index (sweep-1 row ys - R + t),
+    // phase u = t mod NW (compile time after unrolling)
+    auto step = [&](int t, int u) {
+        consume((unsigned)(t + 2 * R), win[(u + 2 * R) % NW]);
+        // sweep 1 at row y1 = ys - R + t, window centred on it
+        const int y1 = ys - R + t;
+        const Win<T, NW, W, R> w{win, u};
+        T s1[V];
+        point_row(w, s1);
+        const bool yint = y1 >= R && y1 < ny - R;
+#pragma unroll
+        for (int p = 0; p < V; ++p)
+            if (!(yint && xin[p])) s1[p] = win[(u + R) % NW][R + p];     // boundary ring: held value
+        T* d = w1[u % NW];
+#pragma unroll
+        for (int k = 0; k < V; ++k) d[R + k] = s1[k];
+        if constexpr (VARIANT == VAR_SHUFFLE) {
+#pragma unroll
+            for (int k = 0; k < R; ++k) d[k] = shfl_up(s1[V - R + k], 1);
+#pragma unroll
+            for (int k = 0; k < R; ++k) d[R + V + k] = shfl_down(s1[k], 1);
+        } else {
+            __syncwarp();                                  // previous row's reads are done
+            stg_vec(srow + lane * V, s1);                  // STS.128 (generic store to smem)
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < R; ++k) d[k] = srow[lane * V - R + k];
+#pragma unroll
+            for (int k = 0; k < R; ++k) d[R + V + k] = srow[lane * V + V + k];
+        }
+        // sweep 2 at row y2 = y1 - R (needs sweep-1 rows y2-R .. y2+R)
+        if (t >= 2 * R) {
+            const int y2 = y1 - R;
+            const Win<T, NW, W, R> w2{w1, (u + 1) % NW};   // centre slot (u - R) mod NW
+            T o[V];
+            point_row(w2, o);
+            T* op = out + (int64_t)y2 * nx + xl;
+            if (vec_store) stg_vec(op, o);
+#pragma unroll
+            for (int p = 0; p < V; ++p)
+                if (el_store[p]) op[p] = o[p];
+        }
+    };
+
+#pragma unroll
+    for (int r = 0; r < 2 * R; ++r) consume((unsigned)r, win[r]);
+    const int nt = ye - ys + 2 * R;                        // sweep-1 rows [ys-R, ye+R)
+    int t = 0;
+    for (; t + NW <= nt; t += NW) {
+#pragma unroll
+        for (int u = 0; u < NW; ++u) step(t + u, u);
+    }
+#pragma unroll
+    for (int u = 0; u < NW - 1; ++u)
+        if (t + u < nt) step(t + u, u);
+}
+
+}  // namespace stb200
