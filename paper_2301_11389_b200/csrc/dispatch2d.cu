@@ -163,7 +163,10 @@ static cudaError_t launch_tb(const stencil_s* h, const void* in, void* out, cuda
 template <class Op, typename T, int VAR>
 static cudaError_t launch_k2d2(const stencil_s* h, const void* in, void* out, cudaStream_t s) {
     constexpr int R = Op::R;
-    constexpr int kStripH = 24;
+    // strip height (measured): the 4R extra input rows of a
+    // strip amortise over tall strips — jacobi2d5 32768^2 fp32 1302 (24) ->
+    // 1459 (128) Gpt/s, flat to 512; fp64 16384^2 best at 48-64
+    constexpr int kStripH = sizeof(T) == 8 ? 64 : 128;
     auto kern = k2d2<Op, T, VAR>;
     constexpr size_t smem = k2d2_smem_bytes<T>();
     static bool attr = false;
