@@ -123,11 +123,11 @@ int stencil_get_variant(stencil_t h, int* variant);
  *                     shared-memory tile kernel (each CTA sweeps its tile plus
  *                     an S*R halo, S as deep as shared memory allows: per-
  *                     launch latency bounds those runs); larger jacobi2d5 /
- *                     jacobi2d9 grids run the streaming two-sweep
- *                     register-cache kernel (one HBM pass per two sweeps:
- *                     the single-sweep kernel is HBM-bound); gaussblur and
- *                     gameoflife keep one sweep per launch (issue-bound at
- *                     two sweeps per pass)
+ *                     jacobi2d9 / gameoflife grids run the streaming
+ *                     two-sweep register-cache kernel (one HBM pass per two
+ *                     sweeps: the single-sweep kernel is HBM-bound);
+ *                     gaussblur keeps one sweep per launch (issue-bound at
+ *                     two sweeps per pass: no gain)
  *   1           never fuse (one sweep per launch)
  *   2           the streaming two-sweep kernel, any grid size
  *   S >= 3      the tile kernel with at most S sweeps per launch

@@ -334,15 +334,17 @@ static int fusion_depth(const stencil_s* h, int n_iters) {
     return 1;
 }
 // Two sweeps per launch through the streaming kernel (k2d2): forced with
-// fusion == 2; automatic for the Jacobi kinds on grids that do not sit in L2.
-// Measured on B200: jacobi2d5 32768^2 fp32 846 -> 1217-1268
-// Gpt/s, jacobi2d9 845 -> 1040, fp64 16384^2 +55-71%; gaussblur (25 FMA/pt)
-// and gameoflife are issue-bound at two sweeps per pass and run slower, so
-// they keep one sweep per launch.
+// fusion == 2; automatic for jacobi2d5 / jacobi2d9 / gameoflife on grids
+// that do not sit in L2.  Measured on B200: jacobi2d5
+// 32768^2 fp32 846 -> 1591 Gpt/s, jacobi2d9 846 -> 1622, gameoflife 16384^2
+// 832 -> 921, fp64 Jacobi 420 -> ~800; gaussblur (25 FMA/pt, issue-bound
+// at two sweeps per pass) is even (805 vs 802) and keeps one sweep per
+// launch.
 static bool pair_fusion(const stencil_s* h, int n_iters) {
     if (!fusable(h) || n_iters < 2) return false;
     if (h->fusion == 2) return true;
-    const bool cheap = h->k->kind == ST_JACOBI2D5 || h->k->kind == ST_JACOBI2D9;
+    const int k = h->k->kind;
+    const bool cheap = k == ST_JACOBI2D5 || k == ST_JACOBI2D9 || k == ST_GAMEOFLIFE;
     return h->fusion == 0 && cheap && !l2_resident(h);
 }
 int stb200::sweeps_per_launch(const stencil_s* h, int n_iters) {

@@ -88,7 +88,7 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
             T* dst0 = ring + (g_lo - (X0 - 2 * V));
             for (int r = 0; r < nrows; ++r) {
                 const unsigned s = (unsigned)r & (S - 1);
-                if (r >= S) mbar_wait_backoff<256>(&empty[s], (((unsigned)r >> LOG2S) - 1) & 1u);
+                if (r >= S) mbar_wait_backoff<512>(&empty[s], (((unsigned)r >> LOG2S) - 1) & 1u);
                 const int yin = row0 + r;
                 if (yin >= 0 && yin < ny) {
                     mbar_arrive_expect_tx(&full[s], bytes);
@@ -169,18 +169,24 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
     };
 
     // one staged input row: t = sweep-1 row index (sweep-1 row ys - R + t),
-    // phase u = t mod NW (compile time after unrolling)
-    auto step = [&](int t, int u) {
+    // phase u = t mod NW (compile time after unrolling).  EDGE = false: the
+    // warp's sweep-1 columns and the strip's sweep-1 rows are all interior
+    // and lanes 1..30 all store whole vectors (no selects, no element
+    // stores); decided once per warp, not per row.
+    auto step = [&](int t, int u, auto edge_tag) {
+        constexpr bool EDGE = decltype(edge_tag)::value;
         consume((unsigned)(t + 2 * R), win[(u + 2 * R) % NW]);
         // sweep 1 at row y1 = ys - R + t, window centred on it
         const int y1 = ys - R + t;
         const Win<T, NW, W, R> w{win, u};
         T s1[V];
         point_row(w, s1);
-        const bool yint = y1 >= R && y1 < ny - R;
+        if constexpr (EDGE) {
+            const bool yint = y1 >= R && y1 < ny - R;
 #pragma unroll
-        for (int p = 0; p < V; ++p)
-            if (!(yint && xin[p])) s1[p] = win[(u + R) % NW][R + p];     // boundary ring: held value
+            for (int p = 0; p < V; ++p)
+                if (!(yint && xin[p])) s1[p] = win[(u + R) % NW][R + p];     // boundary ring: held value
+        }
         T* d = w1[u % NW];
 #pragma unroll
         for (int k = 0; k < V; ++k) d[R + k] = s1[k];
@@ -205,24 +211,37 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
             T o[V];
             point_row(w2, o);
             T* op = out + (int64_t)y2 * nx + xl;
-            if (vec_store) stg_vec(op, o);
+            if constexpr (EDGE) {
+                if (vec_store) stg_vec(op, o);
 #pragma unroll
-            for (int p = 0; p < V; ++p)
-                if (el_store[p]) op[p] = o[p];
+                for (int p = 0; p < V; ++p)
+                    if (el_store[p]) op[p] = o[p];
+            } else {
+                if (own) stg_vec(op, o);
+            }
         }
     };
 
 #pragma unroll
     for (int r = 0; r < 2 * R; ++r) consume((unsigned)r, win[r]);
     const int nt = ye - ys + 2 * R;                        // sweep-1 rows [ys-R, ye+R)
-    int t = 0;
-    for (; t + NW <= nt; t += NW) {
+    auto march = [&](auto edge_tag) {
+        int t = 0;
+        for (; t + NW <= nt; t += NW) {
 #pragma unroll
-        for (int u = 0; u < NW; ++u) step(t + u, u);
-    }
+            for (int u = 0; u < NW; ++u) step(t + u, u, edge_tag);
+        }
 #pragma unroll
-    for (int u = 0; u < NW - 1; ++u)
-        if (t + u < nt) step(t + u, u);
+        for (int u = 0; u < NW - 1; ++u)
+            if (t + u < nt) step(t + u, u, edge_tag);
+    };
+    bool all_x = true;
+#pragma unroll
+    for (int p = 0; p < V; ++p) all_x = all_x && xin[p];
+    const bool rows_inner = ys - R >= R && ye + R <= ny - R;
+    const bool interior = __all_sync(FULL, all_x && (vec_store || lane == 0 || lane == 31)) && rows_inner;
+    if (interior) march(std::false_type{});
+    else march(std::true_type{});
 }
 
 }  // namespace stb200
