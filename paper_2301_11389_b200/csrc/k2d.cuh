@@ -131,7 +131,9 @@ struct OpLife {
         const int e = p + R;
         const int n = w(-1, e - 1) + w(-1, e) + w(-1, e + 1) + w(0, e - 1) + w(0, e + 1)
                     + w(1, e - 1) + w(1, e) + w(1, e + 1);
-        return (n == 3 || (n == 2 && w(0, e) == 1)) ? 1 : 0;
+        // B3/S23 without short-circuit evaluation: no branches (the || / &&
+        // form compiled to divergent branches with BSSY/BSYNC around them)
+        return (int)((n == 3) | ((n == 2) & (w(0, e) == 1)));
     }
 };
 

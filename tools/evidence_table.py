@@ -6,7 +6,9 @@
 Reads profiles/<round>_ncu_summary.md (one ncu --set full launch per
 workload x variant) and profiles/<round>_ops/ops_<w>_<v>.txt (dynamic SASS
 opcode counts, tools/ncu_ops.py).  DRAM / compulsory = (dram read + write)
-/ (interior points x compulsory bytes per point) of that launch.
+/ (interior points x compulsory bytes per point) of that launch; *_pair rows
+are two-sweep k2d2 launches (instr / pt per point of the launch = per two
+sweeps).
 """
 import argparse
 import os
@@ -16,9 +18,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 # interior points of one launch and compulsory bytes per point
 PTS = {"gaussblur": 8188 ** 2, "jacobi2d_paper": 32766 ** 2, "gameoflife": 16382 ** 2,
        "laplacian": 510 ** 3, "wave13pt": 508 ** 3, "jacobi3d": 1022 ** 3, "divergence": 510 ** 3,
-       "gradient": 510 ** 3, "tricubic": 253 ** 3}
+       "gradient": 510 ** 3, "tricubic": 253 ** 3,
+       # two-sweep (k2d2) launches: one read and one write per launch, 2 sweeps
+       "jacobi2d_pair": 32766 ** 2, "gameoflife_pair": 16382 ** 2}
 BPP = {"gaussblur": 8, "jacobi2d_paper": 8, "gameoflife": 8, "laplacian": 16, "wave13pt": 24,
-       "jacobi3d": 8, "divergence": 16, "gradient": 16, "tricubic": 20}
+       "jacobi3d": 8, "divergence": 16, "gradient": 16, "tricubic": 20, "jacobi2d_pair": 8,
+       "gameoflife_pair": 8}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 TSCALE = {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
 
