@@ -349,8 +349,11 @@ def main():
     # the two-sweep kernel (sweeps_per_launch = 2, large jacobi grids) reads
     # its input and writes its output once for two sweeps: its algorithmic
     # bytes per launch are those of one sweep.
-    spl = info["sweeps_per_launch"] if (not attached and iters >= 2 and info["sweeps_per_launch"] == 2) else 1
-    sweep_launches = (iters + 1) // 2 if spl == 2 else iters
+    # (streaming multi-sweep launches are used on grids larger than L2 only;
+    # the L2-resident tile kernel keeps the per-sweep accounting)
+    spl = info["sweeps_per_launch"] if (not attached and iters >= 2 and flush is None
+                                        and info["sweeps_per_launch"] in (2, 3)) else 1
+    sweep_launches = iters // spl + iters % spl
     launches = sweep_launches * info["launches_per_step"]
     avg_launch_s = ms / 1e3 / (args.steps * sweep_launches)   # includes graph gaps: conservative
     alg_bytes = info["bytes_per_point"] * pts_rank              # per launch on this rank
@@ -369,8 +372,8 @@ def main():
         if flush is not None:
             flush.fill_(1.0)
         a.record(stream)
-        if spl == 2:
-            st.run(bufs, 2, stream)          # one two-sweep launch (+ the ring copy)
+        if spl > 1:
+            st.run(bufs, spl, stream)        # one multi-sweep launch (+ the ring copy)
         else:
             st.step(ins, outs, stream)
         b.record(stream)

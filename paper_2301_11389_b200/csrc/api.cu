@@ -340,16 +340,24 @@ static int fusion_depth(const stencil_s* h, int n_iters) {
 // 832 -> 921, fp64 Jacobi 420 -> ~800; gaussblur (25 FMA/pt, issue-bound
 // at two sweeps per pass) is even (805 vs 802) and keeps one sweep per
 // launch.
-static bool pair_fusion(const stencil_s* h, int n_iters) {
-    if (!fusable(h) || n_iters < 2) return false;
-    if (h->fusion == 2) return true;
+// Sweeps per launch of the streaming kernel for a run (0 = not used).
+static int pair_fusion(const stencil_s* h, int n_iters) {
+    if (!fusable(h) || n_iters < 2) return 0;
+    static const int env_nsw = getenv("STB200_2D_NSW") ? atoi(getenv("STB200_2D_NSW")) : 0;
     const int k = h->k->kind;
     const bool cheap = k == ST_JACOBI2D5 || k == ST_JACOBI2D9 || k == ST_GAMEOFLIFE;
-    return h->fusion == 0 && cheap && !l2_resident(h);
+    // three sweeps per launch for jacobi2d5 (measured: 32768^2 fp32 1595 ->
+    // 1792 Gpt/s SHUFFLE, fp64 +8%); jacobi2d9 and gameoflife run slower at
+    // three (issue), gaussblur has no three-sweep kernel
+    int nsw = k == ST_JACOBI2D5 ? 3 : 2;
+    if (cheap && env_nsw >= 2 && env_nsw <= 3) nsw = env_nsw;
+    if (nsw > n_iters) nsw = n_iters;
+    if (h->fusion == 2) return nsw;
+    return h->fusion == 0 && cheap && !l2_resident(h) ? nsw : 0;
 }
 int stb200::sweeps_per_launch(const stencil_s* h, int n_iters) {
-    if (pair_fusion(h, n_iters)) return 2;
-    return fusion_depth(h, n_iters);
+    const int nsw = pair_fusion(h, n_iters);
+    return nsw ? nsw : fusion_depth(h, n_iters);
 }
 
 static int enqueue_run(stencil_s* h, void* const* bufs, int n_iters, cudaStream_t s, int* result) {
@@ -357,20 +365,19 @@ static int enqueue_run(stencil_s* h, void* const* bufs, int n_iters, cudaStream_
     int rc;
     if (dist_is_p2p(h)) return p2p_run(h, bufs, n_iters, s, result);
     if (k->iterable == 1) {
-        if (pair_fusion(h, n_iters)) {
-            // two sweeps per launch (k2d2); an odd count starts with one
-            // single sweep.  The ring stays fixed: copy it once, as below.
+        if (const int nsw = pair_fusion(h, n_iters)) {
+            // nsw sweeps per launch (k2d2); a remainder runs first as single
+            // sweeps.  The ring stays fixed: copy it once, as below.
             if ((rc = ring_copy(h, bufs[0], bufs[1], s))) return rc;
             int cur = 0, done = 0;
-            if (n_iters & 1) {
-                const void* in[1] = {bufs[0]};
-                void* out[1] = {bufs[1]};
+            for (; done < n_iters % nsw; ++done) {
+                const void* in[1] = {bufs[cur]};
+                void* out[1] = {bufs[1 - cur]};
                 if ((rc = launch_sweep(h, in, out, s, -1, -1))) return rc;
-                cur = 1;
-                done = 1;
+                cur = 1 - cur;
             }
-            for (; done < n_iters; done += 2) {
-                cudaError_t e = dispatch_2d_pair(h, bufs[cur], bufs[1 - cur], s);
+            for (; done < n_iters; done += nsw) {
+                cudaError_t e = dispatch_2d_pair(h, bufs[cur], bufs[1 - cur], s, nsw);
                 if (e != cudaSuccess)
                     return set_error(ST_ECUDA, "%s two-sweep launch failed: %s", k->name, cudaGetErrorString(e));
                 cur = 1 - cur;

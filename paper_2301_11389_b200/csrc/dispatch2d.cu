@@ -160,15 +160,15 @@ static cudaError_t launch_tb(const stencil_s* h, const void* in, void* out, cuda
 
 // Two sweeps per launch, streaming (k2d2.cuh): the large-grid form of
 // temporal blocking.  Strips of H sweep-2 rows in blockIdx order, as k2d.
-template <class Op, typename T, int VAR>
+template <class Op, typename T, int VAR, int NSW>
 static cudaError_t launch_k2d2(const stencil_s* h, const void* in, void* out, cudaStream_t s) {
     constexpr int R = Op::R;
-    // strip height (measured): the 4R extra input rows of a
+    // strip height (measured): the extra input rows of a
     // strip amortise over tall strips — jacobi2d5 32768^2 fp32 1302 (24) ->
     // 1459 (128) Gpt/s, flat to 512; fp64 16384^2 best at 48-64
     constexpr int kStripH = sizeof(T) == 8 ? 64 : 128;
-    auto kern = k2d2<Op, T, VAR>;
-    constexpr size_t smem = k2d2_smem_bytes<T>();
+    auto kern = k2d2<Op, T, VAR, NSW>;
+    constexpr size_t smem = k2d2_smem_bytes<T, NSW>();
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -177,7 +177,7 @@ static cudaError_t launch_k2d2(const stencil_s* h, const void* in, void* out, cu
     const int64_t nx = h->ldims[0], ny = h->ldims[1];
     const int64_t y_lo = R, y_hi = ny - R;
     if (y_hi <= y_lo) return cudaSuccess;
-    const int64_t gx = (nx + kWarps2D * k2d2_txo<T>() - 1) / (kWarps2D * k2d2_txo<T>());
+    const int64_t gx = (nx + kWarps2D * k2d2_txo<T, NSW>() - 1) / (kWarps2D * k2d2_txo<T, NSW>());
     const int64_t rows = y_hi - y_lo;
     static const int dbg_h = getenv("STB200_2D2_H") ? atoi(getenv("STB200_2D2_H")) : 0;
     int64_t H = (rows * gx + 2 * sm_count(h->device) - 1) / (2 * sm_count(h->device));
@@ -192,21 +192,30 @@ static cudaError_t launch_k2d2(const stencil_s* h, const void* in, void* out, cu
     return cudaGetLastError();
 }
 
-template <template <typename> class OpT, typename T>
-static cudaError_t pair_var(const stencil_s* h, const void* in, void* out, cudaStream_t s) {
-    if (h->variant == ST_PLAIN) return launch_k2d2<OpT<T>, T, VAR_PLAIN>(h, in, out, s);
-    return launch_k2d2<OpT<T>, T, VAR_SHUFFLE>(h, in, out, s);
+template <class Op, typename T>
+static cudaError_t pair_op(const stencil_s* h, const void* in, void* out, cudaStream_t s, int nsw) {
+    if (h->variant == ST_PLAIN)
+        return nsw == 3 ? launch_k2d2<Op, T, VAR_PLAIN, 3>(h, in, out, s) : launch_k2d2<Op, T, VAR_PLAIN, 2>(h, in, out, s);
+    return nsw == 3 ? launch_k2d2<Op, T, VAR_SHUFFLE, 3>(h, in, out, s) : launch_k2d2<Op, T, VAR_SHUFFLE, 2>(h, in, out, s);
 }
 
-cudaError_t dispatch_2d_pair(stencil_s* h, const void* in, void* out, cudaStream_t s) {
+// nsw sweeps (2 or 3) in one streaming launch (k2d2.cuh)
+cudaError_t dispatch_2d_pair(stencil_s* h, const void* in, void* out, cudaStream_t s, int nsw) {
     const bool f64 = h->dtype == ST_F64;
     switch (h->k->kind) {
-    case ST_JACOBI2D5: return f64 ? pair_var<OpJacobi2D5, double>(h, in, out, s) : pair_var<OpJacobi2D5, float>(h, in, out, s);
-    case ST_JACOBI2D9: return f64 ? pair_var<OpJacobi2D9, double>(h, in, out, s) : pair_var<OpJacobi2D9, float>(h, in, out, s);
-    case ST_GAUSSBLUR5X5: return f64 ? pair_var<OpGauss5, double>(h, in, out, s) : pair_var<OpGauss5, float>(h, in, out, s);
-    case ST_GAMEOFLIFE:
-        if (h->variant == ST_PLAIN) return launch_k2d2<OpLife, int, VAR_PLAIN>(h, in, out, s);
-        return launch_k2d2<OpLife, int, VAR_SHUFFLE>(h, in, out, s);
+    case ST_JACOBI2D5:
+        return f64 ? pair_op<OpJacobi2D5<double>, double>(h, in, out, s, nsw)
+                   : pair_op<OpJacobi2D5<float>, float>(h, in, out, s, nsw);
+    case ST_JACOBI2D9:
+        return f64 ? pair_op<OpJacobi2D9<double>, double>(h, in, out, s, nsw)
+                   : pair_op<OpJacobi2D9<float>, float>(h, in, out, s, nsw);
+    case ST_GAUSSBLUR5X5:   // two sweeps only (issue-bound already at two)
+        if (h->variant == ST_PLAIN)
+            return f64 ? launch_k2d2<OpGauss5<double>, double, VAR_PLAIN, 2>(h, in, out, s)
+                       : launch_k2d2<OpGauss5<float>, float, VAR_PLAIN, 2>(h, in, out, s);
+        return f64 ? launch_k2d2<OpGauss5<double>, double, VAR_SHUFFLE, 2>(h, in, out, s)
+                   : launch_k2d2<OpGauss5<float>, float, VAR_SHUFFLE, 2>(h, in, out, s);
+    case ST_GAMEOFLIFE: return pair_op<OpLife, int>(h, in, out, s, nsw);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -63,7 +63,7 @@ int launch_sweep(stencil_s* h, const void* const* in, void* const* out, cudaStre
 // dispatch2d.cu: temporally blocked 2-D sweeps
 cudaError_t dispatch_2d_fused(stencil_s* h, const void* in, void* out, cudaStream_t s, int S);
 int fused_max_sweeps(const stencil_s* h);
-cudaError_t dispatch_2d_pair(stencil_s* h, const void* in, void* out, cudaStream_t s);
+cudaError_t dispatch_2d_pair(stencil_s* h, const void* in, void* out, cudaStream_t s, int nsw);
 int sweeps_per_launch(const stencil_s* h, int n_iters);
 int ring_copy(const stencil_s* h, const void* src, void* dst, cudaStream_t s);
 

@@ -1,4 +1,4 @@
-// k2d2.cuh — two sweeps per HBM pass for the large 2-D ping-pong runs
+// k2d2.cuh — two (or three) sweeps per HBM pass for the large 2-D ping-pong runs
 // ("multiple sweeps per HBM pass"), register-cache
 // form of k2d.cuh.
 //
@@ -23,31 +23,37 @@
 // work).  A strip of H sweep-2 rows reads H + 4R input rows (the 2R extra
 // rows on each side are shared with the neighbouring strips through L2).
 // Results are bit-identical to two separate k2d sweeps.
+//
+// NSW = 3 chains one more level the same way (sweep-2 rows -> sweep-2
+// register window -> sweep-3 row); each level loses one lane per side, so
+// lanes 2..29 store (28 V columns per warp) and a strip reads H + 6R rows.
 #pragma once
 #include "k2d.cuh"
 
 namespace stb200 {
 
-template <typename T> constexpr int k2d2_txo() { return 30 * vlen<T>(); }       // sweep-2 columns per warp
-template <typename T> constexpr int k2d2_row_elems() { return kWarps2D * k2d2_txo<T>() + 4 * vlen<T>(); }
-template <typename T>
+template <typename T, int NSW = 2> constexpr int k2d2_txo() { return (32 - 2 * (NSW - 1)) * vlen<T>(); }
+template <typename T, int NSW = 2>
+constexpr int k2d2_row_elems() { return kWarps2D * k2d2_txo<T, NSW>() + 2 * NSW * vlen<T>(); }
+template <typename T, int NSW = 2>
 constexpr size_t k2d2_smem_bytes() {
-    return (size_t)kStages2D * (k2d2_row_elems<T>() * sizeof(T) + 2 * sizeof(uint64_t)) +
-           (size_t)kWarps2D * (32 + 2) * vlen<T>() * sizeof(T);        // PLAIN: per-warp sweep-1 row
+    return (size_t)kStages2D * (k2d2_row_elems<T, NSW>() * sizeof(T) + 2 * sizeof(uint64_t)) +
+           (size_t)kWarps2D * (32 + 2) * vlen<T>() * sizeof(T);        // PLAIN: per-warp sweep row
 }
 
-// Grid: x = ceil(nx / (kWarps2D * 30V)), y = strips of H sweep-2 rows
-// covering [y_lo, y_hi) (R <= y_lo, y_hi <= ny - R).
-template <class Op, typename T, int VARIANT>
+// Grid: x = ceil(nx / (kWarps2D * TXO)), y = strips of H output rows
+// covering [y_lo, y_hi) (R <= y_lo, y_hi <= ny - R).  NSW sweeps per launch.
+template <class Op, typename T, int VARIANT, int NSW = 2>
 __global__ void __launch_bounds__(k2d_threads())
 k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo, int y_hi, int H,
      Coeffs<T, Op::NC> c) {
+    static_assert(NSW == 2 || NSW == 3, "two or three sweeps per launch");
     constexpr int R = Op::R;
     constexpr int V = vlen<T>();
-    constexpr int TXO = k2d2_txo<T>();
+    constexpr int TXO = k2d2_txo<T, NSW>();
     constexpr int W = V + 2 * R;
     constexpr int NW = 2 * R + 1;
-    constexpr int WS = k2d2_row_elems<T>();
+    constexpr int WS = k2d2_row_elems<T, NSW>();
     constexpr int S = kStages2D;
     static_assert(R <= V, "halo wider than the staging pad");
     constexpr unsigned LOG2S = S == 2 ? 1 : S == 4 ? 2 : S == 8 ? 3 : S == 16 ? 4 : 5;
@@ -60,12 +66,12 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
 
     const int warp = threadIdx.x >> 5;
     const int lane = lane_id();
-    const int64_t X0 = (int64_t)blockIdx.x * (kWarps2D * TXO);       // CTA's first sweep-2 column
+    const int64_t X0 = (int64_t)blockIdx.x * (kWarps2D * TXO);       // CTA's first output column
     const int ys = y_lo + (int)blockIdx.y * H;
     const int ye = min(ys + H, y_hi);
     if (ys >= ye) return;                                  // CTA-uniform
-    const int row0 = ys - 2 * R;                           // first input row of the strip
-    const int nrows = ye - ys + 4 * R;                     // input rows [ys-2R, ye+2R)
+    const int row0 = ys - NSW * R;                         // first input row of the strip
+    const int nrows = ye - ys + 2 * NSW * R;               // input rows [ys-NSW*R, ye+NSW*R)
     const int64_t n_left = (nx - X0 + TXO - 1) / TXO;
     const int active = n_left < kWarps2D ? (int)n_left : kWarps2D;
 
@@ -80,12 +86,12 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
 
     if (warp == kWarps2D) {                                // ---- producer warp
         if (lane == 0) {
-            // staged element e <-> global column X0 - 2V + e; clip to [0, nx)
-            const int64_t g_lo = X0 - 2 * V > 0 ? X0 - 2 * V : 0;
-            const int64_t g_hi0 = X0 + kWarps2D * TXO + 2 * V;
+            // staged element e <-> global column X0 - NSW*V + e; clip to [0, nx)
+            const int64_t g_lo = X0 - NSW * V > 0 ? X0 - NSW * V : 0;
+            const int64_t g_hi0 = X0 + kWarps2D * TXO + NSW * V;
             const int64_t g_hi = g_hi0 < nx ? g_hi0 : nx;
             const uint32_t bytes = (uint32_t)((g_hi - g_lo) * (int64_t)sizeof(T));
-            T* dst0 = ring + (g_lo - (X0 - 2 * V));
+            T* dst0 = ring + (g_lo - (X0 - NSW * V));
             for (int r = 0; r < nrows; ++r) {
                 const unsigned s = (unsigned)r & (S - 1);
                 if (r >= S) mbar_wait_backoff<512>(&empty[s], (((unsigned)r >> LOG2S) - 1) & 1u);
@@ -103,12 +109,11 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
     if (warp >= active) return;                            // past the row end
 
     // ---- consumer warps
-    const int64_t xs = X0 + (int64_t)warp * TXO - V;       // sweep-1 column of lane 0
+    const int64_t xs = X0 + (int64_t)warp * TXO - (NSW - 1) * V;   // column of lane 0
     const int64_t xl = xs + lane * V;                      // first column of this lane
     const int lo_e = warp * TXO + V + lane * V;            // staged element of column xl
     const bool lane0 = lane == 0, lane31 = lane == 31;
-    T win[NW][W];                                          // input rows
-    T w1[NW][W];                                           // sweep-1 rows
+    T wl[NSW][NW][W];                                      // level 0: input rows; k: sweep-k rows
 
     auto consume = [&](unsigned r, T* dst) {
         const unsigned s = r & (S - 1);
@@ -144,7 +149,7 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
     bool xin[V];
 #pragma unroll
     for (int p = 0; p < V; ++p) xin[p] = xl + p >= R && xl + p < nx - R;
-    const bool own = xl < nx && lane >= 1 && lane <= 30;
+    const bool own = xl < nx && lane >= NSW - 1 && lane <= 32 - NSW;   // lanes whose last sweep is valid
     const bool vec_store = own && xl >= R && xl + V <= nx - R;
     bool el_store[V];
 #pragma unroll
@@ -168,63 +173,71 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
         }
     };
 
-    // one staged input row: t = sweep-1 row index (sweep-1 row ys - R + t),
-    // phase u = t mod NW (compile time after unrolling).  EDGE = false: the
-    // warp's sweep-1 columns and the strip's sweep-1 rows are all interior
-    // and lanes 1..30 all store whole vectors (no selects, no element
-    // stores); decided once per warp, not per row.
-    auto step = [&](int t, int u, auto edge_tag) {
-        constexpr bool EDGE = decltype(edge_tag)::value;
-        consume((unsigned)(t + 2 * R), win[(u + 2 * R) % NW]);
-        // sweep 1 at row y1 = ys - R + t, window centred on it
-        const int y1 = ys - R + t;
-        const Win<T, NW, W, R> w{win, u};
-        T s1[V];
-        point_row(w, s1);
-        if constexpr (EDGE) {
-            const bool yint = y1 >= R && y1 < ny - R;
+    // the x halo of a sweep row from the neighbour lanes
+    auto halo = [&](const T* v, T* d) {
 #pragma unroll
-            for (int p = 0; p < V; ++p)
-                if (!(yint && xin[p])) s1[p] = win[(u + R) % NW][R + p];     // boundary ring: held value
-        }
-        T* d = w1[u % NW];
-#pragma unroll
-        for (int k = 0; k < V; ++k) d[R + k] = s1[k];
+        for (int k = 0; k < V; ++k) d[R + k] = v[k];
         if constexpr (VARIANT == VAR_SHUFFLE) {
 #pragma unroll
-            for (int k = 0; k < R; ++k) d[k] = shfl_up(s1[V - R + k], 1);
+            for (int k = 0; k < R; ++k) d[k] = shfl_up(v[V - R + k], 1);
 #pragma unroll
-            for (int k = 0; k < R; ++k) d[R + V + k] = shfl_down(s1[k], 1);
+            for (int k = 0; k < R; ++k) d[R + V + k] = shfl_down(v[k], 1);
         } else {
             __syncwarp();                                  // previous row's reads are done
-            stg_vec(srow + lane * V, s1);                  // STS.128 (generic store to smem)
+            stg_vec(srow + lane * V, v);                   // STS.128 (generic store to smem)
             __syncwarp();
 #pragma unroll
             for (int k = 0; k < R; ++k) d[k] = srow[lane * V - R + k];
 #pragma unroll
             for (int k = 0; k < R; ++k) d[R + V + k] = srow[lane * V + V + k];
         }
-        // sweep 2 at row y2 = y1 - R (needs sweep-1 rows y2-R .. y2+R)
-        if (t >= 2 * R) {
-            const int y2 = y1 - R;
-            const Win<T, NW, W, R> w2{w1, (u + 1) % NW};   // centre slot (u - R) mod NW
-            T o[V];
-            point_row(w2, o);
-            T* op = out + (int64_t)y2 * nx + xl;
-            if constexpr (EDGE) {
-                if (vec_store) stg_vec(op, o);
+    };
+
+    // one staged input row at step t (phase u = t mod NW, compile time after
+    // unrolling).  Sweep-1 row y1 = ys - (NSW-1)R + t; sweep-k row
+    // y1 - (k-1)R exists once t >= 2R(k-1).  EDGE = false: the warp's columns
+    // and the strip's rows are interior at every level and the storing lanes
+    // all store whole vectors (no selects, no element stores); decided once
+    // per warp, not per row.
+    auto step = [&](int t, int u, auto edge_tag) {
+        constexpr bool EDGE = decltype(edge_tag)::value;
+        consume((unsigned)(t + 2 * R), wl[0][(u + 2 * R) % NW]);
+        const int y1 = ys - (NSW - 1) * R + t;
 #pragma unroll
-                for (int p = 0; p < V; ++p)
-                    if (el_store[p]) op[p] = o[p];
+        for (int k = 1; k <= NSW; ++k) {
+            if (k > 1 && t < 2 * R * (k - 1)) break;
+            const int yk = y1 - (k - 1) * R;
+            // level k-1 window centred on row yk: phase u for the input rows,
+            // (u + 1) mod NW for a sweep level (its row yk was made R steps ago)
+            const int ph = k == 1 ? u : (u + 1) % NW;
+            const Win<T, NW, W, R> w{wl[k - 1], ph};
+            T v[V];
+            point_row(w, v);
+            if (k < NSW) {
+                if constexpr (EDGE) {
+                    const bool yint = yk >= R && yk < ny - R;
+#pragma unroll
+                    for (int p = 0; p < V; ++p)                 // boundary ring: held value
+                        if (!(yint && xin[p])) v[p] = wl[k - 1][(ph + R) % NW][R + p];
+                }
+                halo(v, wl[k][u % NW]);
             } else {
-                if (own) stg_vec(op, o);
+                T* op = out + (int64_t)yk * nx + xl;
+                if constexpr (EDGE) {
+                    if (vec_store) stg_vec(op, v);
+#pragma unroll
+                    for (int p = 0; p < V; ++p)
+                        if (el_store[p]) op[p] = v[p];
+                } else {
+                    if (own) stg_vec(op, v);
+                }
             }
         }
     };
 
 #pragma unroll
-    for (int r = 0; r < 2 * R; ++r) consume((unsigned)r, win[r]);
-    const int nt = ye - ys + 2 * R;                        // sweep-1 rows [ys-R, ye+R)
+    for (int r = 0; r < 2 * R; ++r) consume((unsigned)r, wl[0][r]);
+    const int nt = ye - ys + 2 * (NSW - 1) * R;            // sweep-1 rows
     auto march = [&](auto edge_tag) {
         int t = 0;
         for (; t + NW <= nt; t += NW) {
@@ -238,8 +251,9 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
     bool all_x = true;
 #pragma unroll
     for (int p = 0; p < V; ++p) all_x = all_x && xin[p];
-    const bool rows_inner = ys - R >= R && ye + R <= ny - R;
-    const bool interior = __all_sync(FULL, all_x && (vec_store || lane == 0 || lane == 31)) && rows_inner;
+    const bool stores_lane = lane >= NSW - 1 && lane <= 32 - NSW;
+    const bool rows_inner = ys - (NSW - 1) * R >= R && ye + (NSW - 1) * R <= ny - R;
+    const bool interior = __all_sync(FULL, all_x && (vec_store || !stores_lane)) && rows_inner;
     if (interior) march(std::false_type{});
     else march(std::true_type{});
 }
