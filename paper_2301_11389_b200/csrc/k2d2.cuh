@@ -32,6 +32,10 @@
 
 namespace stb200 {
 
+#ifndef STB200_2D2_FBSEL
+#define STB200_2D2_FBSEL 1        // SHUFFLE fallback as one load + selects (0: predicated asm loads)
+#endif
+
 template <typename T, int NSW = 2> constexpr int k2d2_txo() { return (32 - 2 * (NSW - 1)) * vlen<T>(); }
 template <typename T, int NSW = 2>
 constexpr int k2d2_row_elems() { return kWarps2D * k2d2_txo<T, NSW>() + 2 * NSW * vlen<T>(); }
@@ -133,8 +137,24 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
             for (int k = 0; k < R; ++k) dst[k] = shfl_up(v[V - R + k], 1);
 #pragma unroll
             for (int k = 0; k < R; ++k) dst[R + V + k] = shfl_down(v[k], 1);
+#if STB200_2D2_FBSEL
+            // warp-edge fallback: one load at lane 0's left
+            // or lane 31's right halo address, then selects
+            T e[R];
+            {
+                const T* pe = row + (lane0 ? lo_e - R : lo_e + V);
+#pragma unroll
+                for (int k = 0; k < R; ++k) e[k] = pe[k];
+            }
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                dst[k] = lane0 ? e[k] : dst[k];
+                dst[R + V + k] = lane31 ? e[k] : dst[R + V + k];
+            }
+#else
             lds_pred<T, R>(lane0, row + lo_e - R, dst);     // warp-edge fallback
             lds_pred<T, R>(lane31, row + lo_e + V, dst + R + V);
+#endif
         } else {
 #pragma unroll
             for (int k = 0; k < R; ++k) dst[k] = row[lo_e - R + k];
