@@ -8,7 +8,7 @@ W=${@:-"gaussblur jacobi2d_paper gameoflife laplacian wave13pt jacobi3d divergen
 KEEP=${KEEP:-"prof_tricubic_shuffle"}
 mkdir -p gpurun_out/ncu /tmp/ncu_reps
 for w in $W; do for v in shuffle plain; do
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k2d|k3d|ktricubic' -s 2 -c 1 \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k2d|k3d|ktricubic|kgrad' -s 2 -c 1 \
      -f -o /tmp/ncu_reps/prof_${w}_${v} python tools/prof_run.py --workload $w --variant $v --launches 3 > /dev/null 2>&1 \
      || echo "ncu failed: $w $v"
   python tools/ncu_ops.py /tmp/ncu_reps/prof_${w}_${v}.ncu-rep > gpurun_out/ncu/ops_${w}_${v}.txt 2>&1
