@@ -223,6 +223,7 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
 
     const bool lane0 = lane == 0, lane31 = lane == 31;
     // S2..S4: strip row r -> register window row dst
+    const uint32_t rt_zero = (uint32_t)((uint64_t)nx >> 48);   // 0 at run time, unknown to the compiler
     auto consume = [&](unsigned r, T* dst) {
         const unsigned s = r & (S - 1);
         mbar_wait(&full[s], (r >> LOG2S) & 1u);
@@ -251,7 +252,11 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
 #pragma unroll
             for (int k = 0; k < R; ++k) dst[R + V + k] = row[lo_e + V + k];
         }
-        mbar_arrive(&empty[s]);                           // this lane is done with stage s
+        // release after the loads completed (pipe.cuh mbar_release): one
+        // register of every LDS issued above feeds the (zero) dependency
+        uint32_t dep = bits32(dst[0]) ^ bits32(dst[R - 1]) ^ bits32(dst[R + V]) ^ bits32(dst[R + V + R - 1]) ^
+                       bits32(dst[R]) ^ bits32(dst[R + V - 1]);
+        mbar_release(&empty[s], dep & rt_zero);                           // this lane is done with stage s
     };
 
     // S7 masks: whole-vector store for lanes fully inside the interior, else

@@ -119,6 +119,7 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
     const bool lane0 = lane == 0, lane31 = lane == 31;
     T wl[NSW][NW][W];                                      // level 0: input rows; k: sweep-k rows
 
+    const uint32_t rt_zero = (uint32_t)((uint64_t)nx >> 48);   // 0 at run time, unknown to the compiler
     auto consume = [&](unsigned r, T* dst) {
         const unsigned s = r & (S - 1);
         mbar_wait(&full[s], (r >> LOG2S) & 1u);
@@ -161,7 +162,11 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
 #pragma unroll
             for (int k = 0; k < R; ++k) dst[R + V + k] = row[lo_e + V + k];
         }
-        mbar_arrive(&empty[s]);
+        // release after the loads completed (pipe.cuh mbar_release): one
+        // register of every LDS issued above feeds the (zero) dependency
+        uint32_t dep = bits32(dst[0]) ^ bits32(dst[R - 1]) ^ bits32(dst[R + V]) ^ bits32(dst[R + V + R - 1]) ^
+                       bits32(dst[R]) ^ bits32(dst[R + V - 1]);
+        mbar_release(&empty[s], dep & rt_zero);
     };
 
     // per-element masks: interior columns (sweep 1 computes, else keeps the

@@ -370,14 +370,22 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
             else { v[0] = t.x; v[1] = t.y; }
         };
         // arrival: wait for the plane, push each row's queue-array centre
-        auto arrive_plane = [&](uint32_t gg, int slot, int zplane) {
+        // returns a run-time zero computed from the loaded centres: a release
+        // right after the arrival waits for those loads (pipe.cuh mbar_release)
+        const uint32_t rt_zero = (uint32_t)((uint64_t)args.nx >> 48);
+        auto arrive_plane = [&](uint32_t gg, int slot, int zplane) -> uint32_t {
             (void)zplane;
             mbar_wait(&full[gg % NS], (gg / NS) & 1u);
             const T* b = stage_ptr(gg, Op::QA);
+            uint32_t dep = 0;
 #pragma unroll
-            for (int r = 0; r < RY; ++r) ld_vec(b + off(Op::QA, r, 0, 0), q[r][slot]);
+            for (int r = 0; r < RY; ++r) {
+                ld_vec(b + off(Op::QA, r, 0, 0), q[r][slot]);
+                dep ^= bits32(q[r][slot][0]);
+            }
+            return dep & rt_zero;
         };
-        auto release = [&](uint32_t gg) { mbar_arrive(&empty[gg % NS]); };
+        auto release = [&](uint32_t gg, uint32_t dep) { mbar_release(&empty[gg % NS], dep); };
 
         // in-plane taps of plane gg + compute + store the RY output rows
         auto emit = [&](uint32_t gg, int u) {
@@ -501,7 +509,7 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
                 }
                 bulk_commit();
             }
-            release(gg);
+            release(gg, 0u);                               // after the stores that used every tap
             obase += plane;
             ++zcur;
         };
@@ -511,8 +519,8 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
         // output that reads them in-plane.
 #pragma unroll
         for (int t = 0; t < 2 * R; ++t) {
-            arrive_plane(g + t, t, args.z_lo + zo - R + t);
-            if (t < R || t >= nseg + R) release(g + t);
+            const uint32_t dep = arrive_plane(g + t, t, args.z_lo + zo - R + t);
+            if (t < R || t >= nseg + R) release(g + t, dep);
         }
         // main: arrival t = 2R + i, output i (in-plane plane t - R)
         int i = 0;
@@ -520,8 +528,8 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
 #pragma unroll
             for (int u = 0; u < NQ; ++u) {
                 const uint32_t ga = g + 2 * R + i + u;
-                arrive_plane(ga, (2 * R + u) % NQ, args.z_lo + zo + R + i + u);
-                if (i + u + 2 * R >= np - R) release(ga);  // last R planes: centre only
+                const uint32_t dep = arrive_plane(ga, (2 * R + u) % NQ, args.z_lo + zo + R + i + u);
+                if (i + u + 2 * R >= np - R) release(ga, dep);  // last R planes: centre only
                 emit(ga - R, u);
             }
         }
@@ -529,8 +537,8 @@ k3d(const __grid_constant__ TmapPack<Op::NA> tm, const __grid_constant__ K3Args<
         for (int u = 0; u < NQ - 1; ++u) {
             if (i + u < nseg) {
                 const uint32_t ga = g + 2 * R + i + u;
-                arrive_plane(ga, (2 * R + u) % NQ, args.z_lo + zo + R + i + u);
-                if (i + u + 2 * R >= np - R) release(ga);
+                const uint32_t dep = arrive_plane(ga, (2 * R + u) % NQ, args.z_lo + zo + R + i + u);
+                if (i + u + 2 * R >= np - R) release(ga, dep);
                 emit(ga - R, u);
             }
         }

@@ -164,7 +164,10 @@ ktricubic(const __grid_constant__ TmapPack<1> tm, const __grid_constant__ TriArg
         T* optr = args.out + ((int64_t)(args.z_lo + zo) * args.ny + y) * args.nx + xl;
         auto stage = [&](uint32_t gg) { return smem + (size_t)(gg % NS) * L::STAGE; };
         auto wait = [&](uint32_t gg) { mbar_wait(&full[gg % NS], (gg / NS) & 1u); };
-        auto release = [&](uint32_t gg) { mbar_arrive(&empty[gg % NS]); };
+        // releases carry a zero that depends on the stage's loaded values
+        // (pipe.cuh mbar_release): the arrive waits for those loads
+        const uint32_t rt_zero = (uint32_t)((uint64_t)args.nx >> 48);
+        auto release = [&](uint32_t gg, uint32_t dep) { mbar_release(&empty[gg % NS], dep & rt_zero); };
         auto ldv = [&](const T* p, T* v) {
             using VT = typename VecOf<T>::type;
             const VT t = *reinterpret_cast<const VT*>(p);
@@ -258,7 +261,7 @@ ktricubic(const __grid_constant__ TmapPack<1> tm, const __grid_constant__ TriArg
                 for (int pp = 0; pp < NP; ++pp)
                     sc[pp] = c == 0 ? P::mul(wz[pp][0], sb[pp]) : P::fma(wz[pp][c], sb[pp], sc[pp]);
             }
-            release(g + o);
+            release(g + o, bits32(sc[0].x) ^ bits32(sc[NP - 1].y));
             T ov[V];
 #pragma unroll
             for (int pp = 0; pp < NP; ++pp) { ov[2 * pp] = sc[pp].x; ov[2 * pp + 1] = sc[pp].y; }
@@ -268,9 +271,9 @@ ktricubic(const __grid_constant__ TmapPack<1> tm, const __grid_constant__ TriArg
                 if (x_el[p]) optr[p] = ov[p];
             optr += plane;
         }
-        release(g + nseg);
-        release(g + nseg + 1);
-        release(g + nseg + 2);
+        release(g + nseg, 0u);
+        release(g + nseg + 1, 0u);
+        release(g + nseg + 2, 0u);
         g += nseg + 3;
     }
 }

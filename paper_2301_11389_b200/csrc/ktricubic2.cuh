@@ -233,7 +233,10 @@ ktricubic2(const __grid_constant__ TmapPack<4> tm, const __grid_constant__ TriAr
         float* optr = args.out + ((int64_t)(args.z_lo + zo) * args.ny + y0) * args.nx + xl;
         auto stage = [&](uint32_t gg) { return reinterpret_cast<const float*>(smem + (size_t)(gg % NS) * L::STAGE); };
         auto wait = [&](uint32_t gg) { mbar_wait(&full[gg % NS], (gg / NS) & 1u); };
-        auto release = [&](uint32_t gg) { mbar_arrive(&empty[gg % NS]); };
+        // releases carry a zero that depends on the stage's loaded values
+        // (pipe.cuh mbar_release): the arrive waits for those loads
+        const uint32_t rt_zero = (uint32_t)((uint64_t)args.nx >> 48);
+        auto release = [&](uint32_t gg, uint32_t dep) { mbar_release(&empty[gg % NS], dep & rt_zero); };
 
         wait(g);
         wait(g + 1);
@@ -249,7 +252,8 @@ ktricubic2(const __grid_constant__ TmapPack<4> tm, const __grid_constant__ TriAr
                 ldsv(Yn[0], ob); ldsv(Yn[1], ob + TX);
                 ob += L::O_BYTES / 4;
                 ldsv(Zn[0], ob); ldsv(Zn[1], ob + TX);
-                mbar_arrive(&oempty[go % NO]);
+                mbar_release(&oempty[go % NO], (bits32(Xn[0][0]) ^ bits32(Xn[1][0]) ^ bits32(Yn[0][0]) ^
+                                                bits32(Yn[1][0]) ^ bits32(Zn[0][0]) ^ bits32(Zn[1][0])) & rt_zero);
             }
             // weights of the 4 point pairs (x+p, y0) / (x+p, y0+1).  Row r of a
             // plane (r = 0..4 = y0-1 .. y0+3) enters point y0 with y weight
@@ -330,7 +334,7 @@ ktricubic2(const __grid_constant__ TmapPack<4> tm, const __grid_constant__ TriAr
                     sc[p] = c == 0 ? mul2(wzc, sb[p]) : fma2(wzc, sb[p], sc[p]);
                 }
             }
-            release(g + o);
+            release(g + o, bits32(plo(sc[0])) ^ bits32(phi(sc[0])) ^ bits32(plo(sc[V - 1])) ^ bits32(phi(sc[V - 1])));
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 float ov[V];
@@ -344,9 +348,9 @@ ktricubic2(const __grid_constant__ TmapPack<4> tm, const __grid_constant__ TriAr
             }
             optr += plane;
         }
-        release(g + nseg);
-        release(g + nseg + 1);
-        release(g + nseg + 2);
+        release(g + nseg, 0u);
+        release(g + nseg + 1, 0u);
+        release(g + nseg + 2, 0u);
         g += nseg + 3;
     }
 }

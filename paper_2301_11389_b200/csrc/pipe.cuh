@@ -38,6 +38,27 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Consumer release of a ring stage right after this thread's shared-memory
+// loads from it were ISSUED.  Measured on B200: a plain
+// arrive issued behind in-flight LDS lets the producer's next bulk copy
+// overwrite the stage before those loads read it (PLAIN gaussblur 8192^2
+// x100 differed run to run).  `dep` is 0 at run time but is computed from
+// the loaded registers, so the arrive waits for the loads to complete.
+// STB200_REL (build knob): 2 = data dependency (default), 1 =
+// fence.proxy.async + arrive, 0 = plain arrive (the racy form, A/B only).
+#ifndef STB200_REL
+#define STB200_REL 2
+#endif
+__device__ __forceinline__ void mbar_release(uint64_t* bar, uint32_t dep) {
+    uint32_t a = smem_u32(bar);
+    if (STB200_REL == 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (STB200_REL == 2) a += dep;
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ uint32_t bits32(float x) { return __float_as_uint(x); }
+__device__ __forceinline__ uint32_t bits32(int x) { return (uint32_t)x; }
+__device__ __forceinline__ uint32_t bits32(double x) { return (uint32_t)__double_as_longlong(x); }
+
 // Block until the barrier's phase with the given parity has completed.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(

@@ -168,3 +168,26 @@ def test_config3_gameoflife_16384_x10_windows(oracle):
     for w in wins:
         ref = oracle_window_run(oracle, "gameoflife", "i32", [f, np.zeros_like(f)], 10, w, 1)
         assert_parity(gb[gidx][w], ref, "i32", f"life window {w}")
+
+
+@pytest.mark.slow
+def test_gaussblur_8192_x100_runs_repeat_bit_identically():
+    """Regression for the ring-stage release race: with a
+    plain mbarrier arrive issued behind in-flight shared-memory loads, PLAIN
+    gaussblur 8192^2 x100 differed from run to run (24 of 25 runs in
+    tools/flake_hunt.py).  Every run of either variant must give the same
+    bits (the variants are bit-identical by construction)."""
+    import torch
+    from paper_2301_11389_b200.binding import Stencil
+    f = torch.from_numpy(inputs.generate_np((8192, 8192), "f32", inputs.BASE_SEED + 1)).cuda()
+    ref = None
+    for var in ("shuffle", "plain", "plain", "plain", "shuffle"):
+        st = Stencil("gaussblur5x5", (8192, 8192), "f32", variant=var)
+        bufs = [f.clone(), torch.zeros_like(f)]
+        idx = st.run(bufs, 100)
+        torch.cuda.synchronize()
+        st.close()
+        if ref is None:
+            ref = bufs[idx]
+        else:
+            assert torch.equal(bufs[idx], ref), f"{var}: run differs from the first run"

@@ -223,3 +223,25 @@ def test_suite_single_step_samples(oracle, kind, n):
             m &= ring[sub_in]
             assert_parity(g[m], rr[m], "f32", f"{kind} out{k} window {w}")
     st.close()
+
+
+@pytest.mark.parametrize("dtype,shape", [("f32", (29, 37, 260)), ("f64", (27, 19, 130)),
+                                         ("f32", (3, 3, 4)), ("f32", (20, 3, 132))])
+def test_gradient_kgrad_chunks(oracle, dtype, shape):
+    """kgrad (csrc/kgrad.cuh): z chunks of 8 planes with a ragged last chunk,
+    row groups of 8 with a ragged last group, a ragged x-tile (260 = 2*128+4,
+    130 = 2*64+2) and the degenerate one-plane / one-row cases, element by
+    element against the oracle; SHUFFLE and PLAIN bit-identical."""
+    u = inputs.generate_np(shape, dtype, seed_of("kgrad", dtype, shape))
+    refs = [np.zeros_like(u) for _ in range(3)]
+    oracle.step("gradient", dtype, [u], refs)
+    sl = interior(shape, 1, 1)
+    got = {}
+    for var in ("shuffle", "plain"):
+        gs = gpu_step("gradient", dtype, [u], 3, variant=var, fill=0)
+        for k, (g, r) in enumerate(zip(gs, refs)):
+            assert_parity(g[sl], r[sl], dtype, f"gradient {dtype} {shape} {var} out{k}")
+            assert np.all(g[ring_mask(shape, 1, 1)] == 0), "boundary written"
+        got[var] = gs
+    for a, b in zip(got["shuffle"], got["plain"]):
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), "SHUFFLE and PLAIN differ"
