@@ -260,9 +260,19 @@ def main():
     from paper_2301_11389_b200 import build, inputs
     from paper_2301_11389_b200.binding import Stencil, dist_get_id
 
+    # STB200_BENCH_SHARE_GPU=1 (testing only): every rank on device 0 with a
+    # gloo control plane, so the multi-rank bench path (slab plan, p2p halo
+    # transport, max-over-ranks timing) runs on a one-GPU box; NCCL refuses
+    # two ranks on one device.  Numbers from such a run are not bench values.
+    share = os.environ.get("STB200_BENCH_SHARE_GPU") == "1"
+    if share:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     build.build()                     # no-op when the in-tree .so is current
 
     dims = list(wl["dims"])
