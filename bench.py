@@ -241,6 +241,12 @@ def main():
                     help="run the attached (slab) path even at N=1 (a group of one rank)")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="halo exchange for N>1: fused peer stores over CUDA IPC (default) or NCCL send/recv")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: the slowest axis grows with N (default); strong: the workload's global "
+                         "dims split over the N ranks (SURVEY 8(e): 2-D strong scaling is latency-bound)")
+    ap.add_argument("--slab-of", type=int, default=1,
+                    help="run one rank's share of an N-way strong-scaled slab on this GPU (attached "
+                         "group of one with the slowest axis divided by N): the per-rank latency floor")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
@@ -276,7 +282,10 @@ def main():
     build.build()                     # no-op when the in-tree .so is current
 
     dims = list(wl["dims"])
-    dims[-1] *= world                 # weak scaling along the slowest axis
+    if args.scaling == "weak":
+        dims[-1] *= world             # weak scaling along the slowest axis
+    if args.slab_of > 1:              # one rank's share of an N-way strong-scaled run
+        dims[-1] = dims[-1] // args.slab_of
     st = Stencil(wl["kind"], dims, wl["dtype"], variant=args.variant)
     attached = world > 1 or args.attach
     if attached and args.transport == "nccl":
@@ -488,7 +497,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "Gpoints/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": wl["dtype"], "data": "synthetic (splitmix64 seeded grids, DESIGN.md §6)",
             "config": {"workload": wl["config"], "kind": wl["kind"], "dims": dims,
                        "local_dims": list(ldims), "iters_per_step": iters,
@@ -497,7 +506,8 @@ def main():
                        "transport": args.transport if attached else None,
                        "l2": "flushed between timed steps" if flush is not None
                        else "inputs larger than L2",
-                       "sweeps_per_launch": spl},
+                       "sweeps_per_launch": spl,
+                       "slab_of": args.slab_of if args.slab_of > 1 else None},
             "hbm_gbs": achieved * 1.0,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
