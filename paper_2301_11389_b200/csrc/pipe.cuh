@@ -55,6 +55,13 @@ __device__ __forceinline__ void mbar_release(uint64_t* bar, uint32_t dep) {
     if (STB200_REL == 2) a += dep;
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
+// The same release ordered by a proxy fence instead of a data dependency:
+// the thread's earlier generic-proxy shared-memory reads are ordered before
+// the async-proxy writes the producer issues after this arrival.
+__device__ __forceinline__ void mbar_release_fenced(uint64_t* bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ uint32_t bits32(float x) { return __float_as_uint(x); }
 __device__ __forceinline__ uint32_t bits32(int x) { return (uint32_t)x; }
 __device__ __forceinline__ uint32_t bits32(double x) { return (uint32_t)__double_as_longlong(x); }
