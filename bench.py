@@ -213,7 +213,7 @@ def run_reference(args, wl, world, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Gpoints/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": wl["dtype"], "data": "synthetic (splitmix64, DESIGN.md §6)",
         "config": {"workload": wl["config"], "kind": wl["kind"], "dims": list(wl["dims"]),
                    "iters": wl["iters"]},
