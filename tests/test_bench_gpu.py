@@ -1,0 +1,45 @@
+"""bench.py on the GPU: the default JSON line carries every key of the
+driver contract, and the strong-scaling slab option runs
+the attached path on one rank's share of the grid."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def run_bench(*args):
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True,
+                       text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [l for l in p.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    return json.loads(lines[0])
+
+
+def test_default_line_contract():
+    d = run_bench("--steps", "3", "--warmup", "3", "--cpu-seconds", "1")
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "clocks", "e2e",
+              "gpu_launches", "cpu_baseline"):
+        assert k in d, k
+    assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] == pytest.approx(r["achieved"] / r["peak"])
+    assert d["e2e"]["h2d_bytes_per_step"] == 8192 * 8192 * 4 and d["e2e"]["value"] > 0
+    assert d["gpu_launches"] >= 3 * 100
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["config"]["kind"] == "gaussblur5x5" and d["config"]["dims"] == [8192, 8192]
+
+
+def test_slab_of_strong_share_attached():
+    d = run_bench("--workload", "jacobi3d", "--slab-of", "8", "--attach", "--steps", "2", "--warmup", "3",
+                  "--no-e2e", "--no-cpu-baseline")
+    c = d["config"]
+    assert c["slab_of"] == 8 and c["parallelism"] == "slab1"
+    assert c["dims"] == [1024, 1024, 128] and c["local_dims"] == [1024, 1024, 130]
+    assert d["value"] > 0
