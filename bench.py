@@ -8,8 +8,14 @@ One *step* = one ``stencil_run(n_iters)`` of the workload (Dirichlet ring
 copy + n_iters sweeps, one CUDA graph), i.e. one pass of the whole hot path
 (DESIGN.md §1 rows S1-S9) over one synthetic grid.  Default workload:
 BASELINE.json configs[1], gaussblur 5x5 fp32 8192x8192, 100 iterations;
-for N>1 weak-scaled to 8192 x (8192*N) with a y-slab decomposition and NCCL
-halo exchange.  Prints ONE JSON line (rank 0).
+for N>1 weak-scaled to 8192 x (8192*N) with a y-slab decomposition, one
+process per GPU.  Halo exchange (--transport): p2p (default) = the kernels'
+fused peer stores into the neighbours' buffers over CUDA IPC (NVLink /
+NVSwitch), falling back on every rank to NCCL send/recv when a rank cannot
+map its neighbours' memory; nccl = NCCL send/recv overlapped with the
+interior.  Run directly with --gpus N > 1 (no WORLD_SIZE in the
+environment), bench.py starts the N ranks itself under
+torch.distributed.run.  Prints ONE JSON line (rank 0).
 
 Metric (BASELINE.json): Gpoints/s (interior points x sweeps / s, all ranks)
 and achieved HBM GB/s as a fraction of the measured copy bandwidth.
@@ -149,32 +155,38 @@ class ClockSampler:
 
 
 # --------------------------------------------------------- oracle (CPU)
-def oracle_sample(wl, seconds: float, nthreads: int):
-    """Time the CPU oracle, as it stands, on a bounded crop of the workload.
+_ORACLE_BUFS = {}
 
-    Runs whole sweeps of the oracle on a crop (same generator, same kind,
-    dtype and iteration structure) until `seconds` of wall time pass.
-    Returns (Gpoints/s, description)."""
+
+def oracle_sample(wl, seconds: float, nthreads: int):
+    """Time the CPU oracle, as it stands, on whole sweeps of the workload's
+    full grid (the stated config's dims, same generator, kind, dtype and
+    iteration structure): at least one sweep, then whole sweeps until
+    `seconds` of wall time have passed.  The bounded part is the number of
+    sweeps (a step of the config runs wl["iters"] of them).
+    Returns (Gpoints/s, description, seconds per sweep)."""
     import numpy as np
     from oracle import pyoracle
     from paper_2301_11389_b200 import inputs
 
     kind, dt = wl["kind"], wl["dtype"]
     ar = pyoracle.arity(kind)
-    if len(wl["dims"]) == 2:
-        crop = (min(wl["dims"][1], 2048), min(wl["dims"][0], 2048))
-    else:
-        crop = tuple(min(d, 128) for d in wl["dims"][::-1])
-    seed = inputs.BASE_SEED
-    fields = [inputs.generate_np(crop, dt, seed, a) for a in range(max(ar["n_in"], 1))]
-    if ar["n_bufs"] == 2:
-        bufs = [fields[0], np.zeros_like(fields[0])]
-    elif kind == "wave13pt":
-        bufs = [fields[0], fields[1], np.zeros_like(fields[0])]
-    else:
-        bufs = fields[: ar["n_in"]] + [np.zeros_like(fields[0]) for _ in range(ar["n_out"])]
+    shape = tuple(wl["dims"][::-1])
+    key = (kind, dt, shape)
+    if key not in _ORACLE_BUFS:              # generated once per process
+        seed = inputs.BASE_SEED
+        fields = [inputs.generate_np(shape, dt, seed, a) for a in range(max(ar["n_in"], 1))]
+        if ar["n_bufs"] == 2:
+            bufs = [fields[0], np.zeros_like(fields[0])]
+        elif kind == "wave13pt":
+            bufs = [fields[0], fields[1], np.zeros_like(fields[0])]
+        else:
+            bufs = fields[: ar["n_in"]] + [np.zeros_like(fields[0]) for _ in range(ar["n_out"])]
+        _ORACLE_BUFS.clear()
+        _ORACLE_BUFS[key] = bufs
+    bufs = _ORACLE_BUFS[key]
     interior = 1
-    for n in crop:
+    for n in shape:
         interior *= n - ar["lo"] - ar["hi"]
     sweeps, t0 = 0, time.perf_counter()
     while True:
@@ -183,8 +195,10 @@ def oracle_sample(wl, seconds: float, nthreads: int):
         el = time.perf_counter() - t0
         if el >= seconds:
             break
-    return interior * sweeps / el / 1e9, (f"{kind} {dt} crop {'x'.join(map(str, crop[::-1]))}, "
-                                          f"{sweeps} sweeps in {el:.1f} s, {nthreads} threads")
+    return (interior * sweeps / el / 1e9,
+            f"{kind} {dt} full grid {'x'.join(map(str, wl['dims']))}: {sweeps} whole sweep(s) of the "
+            f"config's {wl['iters']} in {el:.2f} s, {nthreads} thread(s)",
+            el / sweeps)
 
 
 def host_cores():
@@ -196,18 +210,24 @@ def host_cores():
 
 # ------------------------------------------------------------ reference
 def run_reference(args, wl, world, rank):
+    """The reference arm: the oracle as it stands on this host's cores.  Each
+    step runs whole sweeps of the config's full grid for a bounded time
+    (the whole run stays within a few minutes); ms_per_step is the wall time
+    of those sweeps and `value` the same Gpoints/s metric."""
     if rank != 0:
         return
     cores = host_cores()
-    per_step = max(2.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    per_step = max(1.0, min(10.0, 100.0 / max(1, args.steps + args.warmup)))
+    oracle_sample(wl, 0.0, cores)            # generate the grid, one untimed sweep
     for _ in range(args.warmup):
         oracle_sample(wl, per_step / 4, cores)
-    vals, descs = [], []
+    vals, descs, t_sweep = [], [], []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        v, d = oracle_sample(wl, per_step, cores)
+        v, d, ts = oracle_sample(wl, per_step, cores)
         vals.append(v)
         descs.append(d)
+        t_sweep.append(ts)
     el = time.perf_counter() - t0
     value = sum(vals) / len(vals)
     line = {
@@ -216,7 +236,10 @@ def run_reference(args, wl, world, rank):
         "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": wl["dtype"], "data": "synthetic (splitmix64, DESIGN.md §6)",
         "config": {"workload": wl["config"], "kind": wl["kind"], "dims": list(wl["dims"]),
-                   "iters": wl["iters"]},
+                   "iters": wl["iters"],
+                   "step": "a bounded sample of the config's step: whole sweeps of its full grid "
+                           f"(~{per_step:.0f} s); one whole config step ({wl['iters']} sweeps) "
+                           f"would take {sum(t_sweep) / len(t_sweep) * wl['iters']:.1f} s"},
         "cpu_baseline": {"value": value, "unit": "Gpoints/s", "cores": cores, "kind": "oracle",
                          "sample": descs[-1]},
         "e2e": {"value": value, "unit": "Gpoints/s", "h2d_bytes_per_step": 0,
@@ -226,6 +249,76 @@ def run_reference(args, wl, world, rank):
 
 
 # ------------------------------------------------------------------ ours
+def relaunch(n: int) -> int:
+    """Re-run this command as n ranks under torch.distributed.run (127.0.0.1
+    rendezvous on a free port); returns the launcher's exit code."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd, env=dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1")))
+
+
+def attach_transport(args, st_factory, rank, world, dist, torch, dist_get_id):
+    """Attach a handle for the slab decomposition.  p2p (fused peer stores)
+    is tried first when asked for; if any rank cannot use it (no peer
+    access between the GPUs, no stream memory operations: ST_EUNSUPPORTED
+    from stencil_dist_attach_p2p / stencil_p2p_import), every rank falls back
+    to NCCL send/recv together.  Returns (handle, transport, register) where
+    register(bufs) finishes the p2p setup (a no-op for NCCL)."""
+    from paper_2301_11389_b200.binding import StencilError
+
+    def agree(ok: bool) -> bool:            # all ranks must take the same transport
+        if world == 1:
+            return ok
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32,
+                         device="cpu" if dist.get_backend() == "gloo" else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return bool(t.item())
+
+    def allgather(blob):
+        if world == 1:
+            return [blob]
+        parts = [None] * world
+        dist.all_gather_object(parts, blob)
+        return parts
+
+    if args.transport == "p2p":
+        st = st_factory()
+        ok, why = True, None
+        try:
+            st.attach_p2p(rank, world)
+        except StencilError as e:
+            ok, why = False, str(e)
+        if agree(ok):
+            def register(bufs):
+                try:
+                    st.p2p_register(bufs, allgather)
+                    good = True
+                except StencilError as e:
+                    sys.stderr.write(f"rank {rank}: p2p import failed: {e}\n")
+                    good = False
+                return agree(good)
+            return st, "p2p", register
+        if why:
+            sys.stderr.write(f"rank {rank}: p2p attach failed ({why}); falling back to NCCL\n")
+        st.close()
+    st = st_factory()
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(dist_get_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        st.attach(bytes(uid.cpu().tolist()), rank, world)
+    else:                         # the multi-GPU code path with a group of one
+        st.attach(dist_get_id(), 0, 1)
+    return st, "nccl", lambda bufs: True
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -252,14 +345,21 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        # launched directly with --gpus N: start the N ranks ourselves (one
+        # process per GPU, the same torch.distributed.run launch the driver
+        # uses); rank 0 prints the one JSON line
+        sys.exit(relaunch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     wl = dict(WORKLOADS[args.workload])
 
     if args.impl == "reference":
-        run_reference(args, wl, world, rank)
+        run_reference(args, wl, max(world, args.gpus), rank)
         return
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     import torch
     import torch.distributed as dist
@@ -286,19 +386,15 @@ def main():
         dims[-1] *= world             # weak scaling along the slowest axis
     if args.slab_of > 1:              # one rank's share of an N-way strong-scaled run
         dims[-1] = dims[-1] // args.slab_of
-    st = Stencil(wl["kind"], dims, wl["dtype"], variant=args.variant)
     attached = world > 1 or args.attach
-    if attached and args.transport == "nccl":
-        if world > 1:
-            uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
-            if rank == 0:
-                uid.copy_(torch.frombuffer(bytearray(dist_get_id()), dtype=torch.uint8))
-            dist.broadcast(uid, 0)
-            st.attach(bytes(uid.cpu().tolist()), rank, world)
-        else:                         # the multi-GPU code path with a group of one
-            st.attach(dist_get_id(), 0, 1)
-    elif attached:
-        st.attach_p2p(rank, world)
+    transport = None
+    register = None
+    if attached:
+        st, transport, register = attach_transport(
+            args, lambda: Stencil(wl["kind"], dims, wl["dtype"], variant=args.variant), rank, world,
+            dist, torch, dist_get_id)
+    else:
+        st = Stencil(wl["kind"], dims, wl["dtype"], variant=args.variant)
     info = st.info()
     n_in, n_out, n_bufs = st.arity()
     ldims = info["local_dims"][: len(dims)]
@@ -313,14 +409,13 @@ def main():
         bufs = [fields[0], fields[1], torch.zeros_like(fields[0])]
     else:
         bufs = fields + [torch.zeros_like(fields[0]) for _ in range(n_out)]
-    if attached and args.transport == "p2p":
-        def allgather(blob):
-            if world == 1:
-                return [blob]
-            parts = [None] * world
-            dist.all_gather_object(parts, blob)
-            return parts
-        st.p2p_register(bufs, allgather)
+    if attached and not register(bufs):
+        # a rank could not map its neighbours' buffers: every rank re-attaches with NCCL
+        st.close()
+        args.transport = "nccl"
+        st, transport, register = attach_transport(
+            args, lambda: Stencil(wl["kind"], dims, wl["dtype"], variant=args.variant), rank, world,
+            dist, torch, dist_get_id)
     nbytes_buf = bufs[0].numel() * bufs[0].element_size()
     flush = None
     if nbytes_buf * len(bufs) < 2 * L2_BYTES:
@@ -490,8 +585,10 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = host_cores()
-        v, desc = oracle_sample(wl, args.cpu_seconds, cores)
-        cpu = {"value": v, "unit": "Gpoints/s", "cores": cores, "kind": "oracle", "sample": desc}
+        v, desc, _ = oracle_sample(wl, args.cpu_seconds, cores)
+        v1, desc1, _ = oracle_sample(wl, args.cpu_seconds / 3, 1)
+        cpu = {"value": v, "unit": "Gpoints/s", "cores": cores, "kind": "oracle", "sample": desc,
+               "single_thread": {"value": v1, "unit": "Gpoints/s", "cores": 1, "sample": desc1}}
 
     if rank == 0:
         line = {
@@ -503,7 +600,7 @@ def main():
                        "local_dims": list(ldims), "iters_per_step": iters,
                        "variant": args.variant,
                        "parallelism": (f"slab{world}" if world > 1 else "slab1") if attached else "1gpu",
-                       "transport": args.transport if attached else None,
+                       "transport": transport,
                        "l2": "flushed between timed steps" if flush is not None
                        else "inputs larger than L2",
                        "sweeps_per_launch": spl,

@@ -120,21 +120,25 @@ int stencil_get_variant(stencil_t h, int* variant);
  * apply several sweeps per kernel launch; results are bit-identical to
  * single sweeps.
  *   0 (default) auto: grids that sit in L2 (<= 8 MiB per buffer) run the
- *                     shared-memory tile kernel (each CTA sweeps its tile plus
- *                     an S*R halo, S as deep as shared memory allows: per-
- *                     launch latency bounds those runs); larger jacobi2d5 /
- *                     jacobi2d9 / gameoflife grids run the streaming
- *                     two-sweep register-cache kernel (one HBM pass per two
- *                     sweeps: the single-sweep kernel is HBM-bound);
- *                     gaussblur keeps one sweep per launch (issue-bound at
- *                     two sweeps per pass: no gain)
+ *                     on-chip kernels (per-launch latency bounds those runs);
+ *                     larger jacobi2d5 grids run the streaming three-sweep
+ *                     register-cache kernel, jacobi2d9 / gameoflife the
+ *                     two-sweep one (one HBM pass per two or three sweeps:
+ *                     the single-sweep kernel is HBM-bound); gaussblur keeps
+ *                     one sweep per launch (issue-bound at two sweeps per
+ *                     pass: no gain)
  *   1           never fuse (one sweep per launch)
- *   2           the streaming two-sweep kernel, any grid size
- *   S >= 3      the tile kernel with at most S sweeps per launch
- * Only the register-cache variants (SHUFFLE/PLAIN) and single-GPU handles
- * fuse; stencil_step is always one sweep.  The result buffer of a run is
- * reported in *result_idx (fused runs may differ from n_iters % 2); the
- * other buffer holds an earlier sweep. */
+ *   2           the streaming kernel with exactly two sweeps per launch
+ *   3           the streaming kernel with exactly three sweeps per launch
+ *               (jacobi2d5 / jacobi2d9 / gameoflife; ST_EUNSUPPORTED for
+ *               gaussblur5x5)
+ *   -S (S >= 2) the shared-memory tile kernel, at most S sweeps per launch
+ * A run whose sweep count is not a multiple of the streaming depth runs the
+ * remainder as single sweeps first.  Anything else: ST_EARG.  Only the
+ * register-cache variants (SHUFFLE/PLAIN) and single-GPU handles fuse;
+ * stencil_step is always one sweep.  The result buffer of a run is reported
+ * in *result_idx (fused runs may differ from n_iters % 2); the other buffer
+ * holds an earlier sweep. */
 int stencil_set_fusion(stencil_t h, int sweeps_per_launch);
 
 /* Arity: inputs and outputs of one step; buffers stencil_run expects
@@ -151,7 +155,7 @@ typedef struct {
     double bytes_per_point;   /* compulsory HBM bytes per interior point per step   */
     int launches_per_step;    /* kernels one stencil_step enqueues                  */
     int sweeps_per_launch;    /* sweeps per sweep-kernel launch of a long stencil_run
-                                 on this handle (1, 2 = streaming pair, S = tile)   */
+                                 on this handle (1, 2 / 3 = streaming, S = tile)   */
     int rank, nranks;         /* 0,1 unless attached                                */
 } stencil_info_t;
 int stencil_info(stencil_t h, stencil_info_t* out);

@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -78,6 +79,25 @@ static void default_coeffs(int kind, double* c) {
     }
 }
 
+int stb200::kernel_setup(const void* func, int device, size_t smem, int threads) {
+    struct Entry { size_t smem; int bps; };
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, Entry> done;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = done.find({func, device});
+    if (it != done.end() && it->second.smem >= smem) return it->second.bps;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != device) cudaSetDevice(device);
+    cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int bps = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, func, threads, smem) != cudaSuccess || bps < 1)
+        bps = 1;
+    if (prev >= 0 && prev != device) cudaSetDevice(prev);
+    done[{func, device}] = Entry{smem, bps};
+    return bps;
+}
+
 static size_t dtype_size(int dt) { return dt == ST_F64 ? 8 : 4; }
 
 // ------------------------------------------------------------- lifecycle
@@ -140,7 +160,11 @@ extern "C" int stencil_set_variant(stencil_t h, int variant) {
 
 extern "C" int stencil_set_fusion(stencil_t h, int sweeps_per_launch) {
     if (!h) return set_error(ST_EARG, "null handle");
-    if (sweeps_per_launch < 0 || sweeps_per_launch > 64) return set_error(ST_EARG, "bad fusion depth");
+    if (sweeps_per_launch < -64 || sweeps_per_launch > 3 || sweeps_per_launch == -1)
+        return set_error(ST_EARG, "bad fusion setting %d (0 auto, 1 off, 2 / 3 streaming, -S tile)",
+                         sweeps_per_launch);
+    if (sweeps_per_launch == 3 && h->k->kind == ST_GAUSSBLUR5X5)
+        return set_error(ST_EUNSUPPORTED, "gaussblur5x5 has no three-sweep streaming kernel");
     h->fusion = sweeps_per_launch;
     for (auto& g : h->graphs)          // cached graphs encode the old schedule
         if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -329,7 +353,7 @@ static bool l2_resident(const stencil_s* h) {
 static int fusion_depth(const stencil_s* h, int n_iters) {
     if (!fusable(h) || n_iters < 2) return 1;
     const int smax = fused_max_sweeps(h);
-    if (h->fusion >= 3) return h->fusion < smax ? h->fusion : smax;
+    if (h->fusion <= -2) return -h->fusion < smax ? -h->fusion : smax;
     if (h->fusion == 0 && l2_resident(h)) return smax;
     return 1;
 }
@@ -351,8 +375,9 @@ static int pair_fusion(const stencil_s* h, int n_iters) {
     // three (issue), gaussblur has no three-sweep kernel
     int nsw = k == ST_JACOBI2D5 ? 3 : 2;
     if (cheap && env_nsw >= 2 && env_nsw <= 3) nsw = env_nsw;
+    if (h->fusion == 2 || h->fusion == 3) nsw = h->fusion;   // forced: exactly that many
     if (nsw > n_iters) nsw = n_iters;
-    if (h->fusion == 2) return nsw;
+    if (h->fusion == 2 || h->fusion == 3) return nsw;
     return h->fusion == 0 && cheap && !l2_resident(h) ? nsw : 0;
 }
 int stb200::sweeps_per_launch(const stencil_s* h, int n_iters) {

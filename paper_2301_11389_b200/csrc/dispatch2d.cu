@@ -37,11 +37,7 @@ static cudaError_t launch_k2d(const stencil_s* h, const void* in, void* out, cud
     if (!FUSED && (h->peer_lo || h->peer_hi)) return launch_k2d<Op, T, VAR, true>(h, in, out, s, y_lo, y_hi);
     auto kern = k2d<Op, T, VAR, FUSED>;
     constexpr size_t smem = k2d_smem_bytes<T>();
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    kernel_setup((const void*)kern, h->device, smem, k2d_threads());
     const int64_t nx = h->ldims[0], ny = h->ldims[1];
     if (y_lo < 0) { y_lo = R; y_hi = ny - R; }
     if (y_hi <= y_lo) return cudaSuccess;
@@ -145,11 +141,7 @@ static cudaError_t launch_tb(const stencil_s* h, const void* in, void* out, cuda
     const int64_t nx = h->ldims[0], ny = h->ldims[1];
     const int hh = S * R;
     const size_t smem = 2 * (size_t)(kTbTileX + 2 * hh) * (kTbTileY + 2 * hh) * sizeof(T);
-    static size_t attr = 0;
-    if (smem > attr) {
-        cudaFuncSetAttribute(ktb2d<Op, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = smem;
-    }
+    kernel_setup((const void*)ktb2d<Op, T>, h->device, smem, kTbThreads);
     const dim3 grid((unsigned)((nx - 2 * R + kTbTileX - 1) / kTbTileX),
                     (unsigned)((ny - 2 * R + kTbTileY - 1) / kTbTileY));
     Coeffs<T, Op::NC> c{};
@@ -169,11 +161,7 @@ static cudaError_t launch_k2d2(const stencil_s* h, const void* in, void* out, cu
     constexpr int kStripH = sizeof(T) == 8 ? 64 : 128;
     auto kern = k2d2<Op, T, VAR, NSW>;
     constexpr size_t smem = k2d2_smem_bytes<T, NSW>();
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    kernel_setup((const void*)kern, h->device, smem, k2d_threads());
     const int64_t nx = h->ldims[0], ny = h->ldims[1];
     const int64_t y_lo = R, y_hi = ny - R;
     if (y_hi <= y_lo) return cudaSuccess;

@@ -63,13 +63,7 @@ static cudaError_t launch_k3d(const stencil_s* h, const void* const* in, void* c
     if (!FUSED && (h->peer_lo || h->peer_hi)) return launch_k3d<Op, T, VAR, true>(h, in, out, s, z_lo, z_hi);
     auto kern = k3d<Op, T, VAR, FUSED>;
     constexpr size_t smem = L::smem_bytes();
-    static int blocks_per_sm = 0;
-    if (!blocks_per_sm) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, k3d_threads(), smem) !=
-                cudaSuccess || blocks_per_sm < 1)
-            blocks_per_sm = 1;
-    }
+    const int blocks_per_sm = kernel_setup((const void*)kern, h->device, smem, k3d_threads());
     const int64_t* ld = h->ldims;
     if (z_lo < 0) { z_lo = Op::R; z_hi = ld[2] - Op::R; }
     if (z_hi <= z_lo) return cudaSuccess;
@@ -251,11 +245,7 @@ static cudaError_t launch_tri(const stencil_s* h, const void* const* in, void* c
                               int64_t z_lo, int64_t z_hi) {
     using L = TriLayout<T>;
     auto kern = ktricubic<T, VAR>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
-        attr = true;
-    }
+    kernel_setup((const void*)kern, h->device, L::SMEM, (kTriWarps + 1) * 32);
     const int64_t* ld = h->ldims;
     if (z_lo < 0) { z_lo = 1; z_hi = ld[2] - 2; }
     if (z_hi <= z_lo) return cudaSuccess;
@@ -294,11 +284,7 @@ static cudaError_t launch_tri2(const stencil_s* h, const void* const* in, void* 
                                int64_t z_lo, int64_t z_hi) {
     using L = Tri2Layout;
     auto kern = ktricubic2<VAR>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
-        attr = true;
-    }
+    kernel_setup((const void*)kern, h->device, L::SMEM, (kTri2Warps + 1) * 32);
     const int64_t* ld = h->ldims;
     if (z_lo < 0) { z_lo = 1; z_hi = ld[2] - 2; }
     if (z_hi <= z_lo) return cudaSuccess;

@@ -182,20 +182,31 @@ int dist_step(stencil_s* h, const void* const* in, void* const* out, cudaStream_
     const int64_t recv_lo_at = d->plan[3], send_lo_from = d->plan[4];
     const int64_t recv_hi_at = d->plan[5], send_hi_from = d->plan[6];
     const size_t n_lo = (size_t)(d->plan[7] & 0xFFFF), n_hi = (size_t)(d->plan[7] >> 16);
+    // a failed enqueue still closes the group (NCCL requires balanced
+    // GroupStart / GroupEnd) before the first error is returned
+    int first = ST_OK;
+    auto chk = [&](ncclResult_t r, const char* what) {
+        if (r != 0 && first == ST_OK) first = nccl_check(r, what);
+    };
     for (int ai = 0; ai < h->k->n_in; ++ai) {
         if (!(mask >> ai & 1u)) continue;
         char* buf = (char*)in[ai];     // the halo planes of an input are the exchange's
         if (has_lower) {               // my bottom hi owned planes <-> rank-1's top lo planes
-            api.Send(buf + (size_t)send_lo_from * pb, n_hi * pb, kNcclInt8, h->rank - 1, d->comm, d->comm_stream);
-            api.Recv(buf + (size_t)recv_lo_at * pb, n_lo * pb, kNcclInt8, h->rank - 1, d->comm, d->comm_stream);
+            chk(api.Send(buf + (size_t)send_lo_from * pb, n_hi * pb, kNcclInt8, h->rank - 1, d->comm,
+                         d->comm_stream), "ncclSend to rank-1");
+            chk(api.Recv(buf + (size_t)recv_lo_at * pb, n_lo * pb, kNcclInt8, h->rank - 1, d->comm,
+                         d->comm_stream), "ncclRecv from rank-1");
         }
         if (has_upper) {               // my top lo owned planes <-> rank+1's bottom hi planes
-            api.Send(buf + (size_t)send_hi_from * pb, n_lo * pb, kNcclInt8, h->rank + 1, d->comm, d->comm_stream);
-            api.Recv(buf + (size_t)recv_hi_at * pb, n_hi * pb, kNcclInt8, h->rank + 1, d->comm,
-                     d->comm_stream);
+            chk(api.Send(buf + (size_t)send_hi_from * pb, n_lo * pb, kNcclInt8, h->rank + 1, d->comm,
+                         d->comm_stream), "ncclSend to rank+1");
+            chk(api.Recv(buf + (size_t)recv_hi_at * pb, n_hi * pb, kNcclInt8, h->rank + 1, d->comm,
+                         d->comm_stream), "ncclRecv from rank+1");
         }
     }
-    if ((rc = nccl_check(api.GroupEnd(), "ncclGroupEnd"))) return rc;
+    rc = nccl_check(api.GroupEnd(), "ncclGroupEnd");
+    if (first) return first;
+    if (rc) return rc;
     if ((e = cudaEventRecord(d->e_comm, d->comm_stream)) != cudaSuccess)
         return set_error(ST_ECUDA, "event: %s", cudaGetErrorString(e));
 
@@ -223,10 +234,15 @@ void dist_release(stencil_s* h) {
 
 // Full-plane ranges of the Dirichlet ring copy in local slow-axis planes.
 void dist_ring_planes(const stencil_s* h, int64_t* full_lo, int64_t* full_hi) {
+    // local plane L holds global plane rank*m - lo + L; global planes < lo and
+    // >= n - hi are the Dirichlet boundary.  They are copied whole: rank 0's
+    // dead + boundary planes, the last rank's, and (slabs thinner than 2*lo
+    // or 2*hi) boundary planes that sit in a middle rank's halo, which no
+    // rank computes and the fused peer stores therefore never refresh.
     const int lo = h->k->lo, hi = h->k->hi;
-    const int64_t m = h->dist->m;
-    *full_lo = h->rank == 0 ? 2 * lo : 0;                        // dead + boundary planes
-    *full_hi = h->rank == h->nranks - 1 ? lo + m - hi : lo + m + hi;
+    const int64_t m = h->dist->m, base = (int64_t)h->rank * m;
+    *full_lo = std::max<int64_t>(0, 2 * lo - base);
+    *full_hi = std::min<int64_t>(lo + m + hi, h->dist->n - hi - base + lo);
 }
 
 }  // namespace stb200

@@ -51,6 +51,12 @@ struct stencil_s {
 namespace stb200 {
 
 int set_error(int code, const char* fmt, ...);
+// Per (kernel, device) one-time setup, thread-safe: opts the kernel in to
+// `smem` bytes of dynamic shared memory on `device` (the attribute is per
+// device context, so a handle on a second GPU needs its own call) and
+// returns its resident blocks per SM at (threads, smem), >= 1.  A later
+// call with a larger smem re-applies the attribute.  api.cu.
+int kernel_setup(const void* func, int device, size_t smem, int threads);
 const KindInfo* kind_info(int kind);
 int64_t interior_points(const stencil_s* h);
 

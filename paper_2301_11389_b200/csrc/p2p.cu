@@ -42,6 +42,7 @@ struct P2PState {
     uint32_t* flags = nullptr;         // mine: done, ready_lo, ready_hi
     uint32_t* pflags[2] = {nullptr, nullptr};
     uint32_t epoch = 0;
+    unsigned wait_flags = CU_STREAM_WAIT_VALUE_GEQ;   // | FLUSH where the device supports it
     std::vector<PeerSet> sets;
     std::map<std::string, char*> opened;   // IPC handle bytes -> mapped base
 };
@@ -74,8 +75,11 @@ static DrvApi& drv() {
     return a;
 }
 
-static int wait_geq(cudaStream_t s, const uint32_t* addr, uint32_t v) {
-    CUresult r = drv().wait((CUstream)s, (CUdeviceptr)addr, v, CU_STREAM_WAIT_VALUE_GEQ);
+// flags: CU_STREAM_WAIT_VALUE_GEQ, plus CU_STREAM_WAIT_VALUE_FLUSH (flush the
+// remote writes that arrived before the flag) where the device supports it.
+static int wait_geq(cudaStream_t s, const uint32_t* addr, uint32_t v,
+                    unsigned flags = CU_STREAM_WAIT_VALUE_GEQ) {
+    CUresult r = drv().wait((CUstream)s, (CUdeviceptr)addr, v, flags);
     return r == CUDA_SUCCESS ? ST_OK : set_error(ST_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
 }
 static int write_val(cudaStream_t s, uint32_t* addr, uint32_t v) {
@@ -130,7 +134,7 @@ static int exchange_inputs(stencil_s* h, const PeerSet* ps, int k, cudaStream_t 
         if ((rc = write_val(s, p->pflags[q] + (q == 0 ? 2 : 1), sig))) return rc;
     }
     for (int q = 0; q < 2; ++q)
-        if (has[q] && (rc = wait_geq(s, p->flags + 1 + q, sig))) return rc;
+        if (has[q] && (rc = wait_geq(s, p->flags + 1 + q, sig, p->wait_flags))) return rc;
     return ST_OK;
 }
 
@@ -209,13 +213,21 @@ int p2p_run(stencil_s* h, void* const* bufs, int n_iters, cudaStream_t s, int* r
 
     int idx[3] = {0, 1, 2};            // ping-pong (cur, next) or wave (prev, cur, next)
     const int cur0 = k->iterable == 1 ? 0 : 1;
+    // prologue: the current field's halo planes from the neighbours first
+    // (exchange_inputs returns once mine have arrived), then the Dirichlet
+    // ring into the other run buffer(s).  In those buffers the fused peer
+    // stores write only the interior columns of the halo planes, so the
+    // x-edge (and, in 3-D, y-edge) cells of the halo planes come from this
+    // ring copy, i.e. from the neighbours' values: the corner taps of the box
+    // stencils read them.  Copying before the exchange arrived would
+    // propagate whatever the caller left in the current field's halo planes.
+    if ((rc = exchange_inputs(h, ps, cur0, s, done_prev, base + 1))) return rc;
     if (k->iterable == 1) {
         if ((rc = ring_copy(h, bufs[0], bufs[1], s))) return rc;
     } else {
         if ((rc = ring_copy(h, bufs[1], bufs[0], s))) return rc;
         if ((rc = ring_copy(h, bufs[1], bufs[2], s))) return rc;
     }
-    if ((rc = exchange_inputs(h, ps, cur0, s, done_prev, base + 1))) return rc;   // prologue
     p->epoch = base;
     if ((rc = write_val(s, p->flags, base))) return rc;
     for (int it = 0; it < n_iters; ++it) {
@@ -224,7 +236,7 @@ int p2p_run(stencil_s* h, void* const* bufs, int n_iters, cudaStream_t s, int* r
         const int io = k->iterable == 1 ? idx[1] : idx[2];
         for (int q = 0; q < 2; ++q)
             if (has[q]) {
-                if ((rc = wait_geq(s, p->flags + 1 + q, e))) return rc;     // my input halos
+                if ((rc = wait_geq(s, p->flags + 1 + q, e, p->wait_flags))) return rc;   // my input halos
                 if ((rc = wait_geq(s, p->pflags[q], e - 1))) return rc;    // q's output buffer free
             }
         // fused stores of the output's boundary planes into the neighbours
@@ -267,11 +279,18 @@ constexpr uint32_t kBlobMagic = 0x53503250u;   // "P2PS"
 extern "C" int stencil_dist_attach_p2p(stencil_t h, int rank, int nranks) {
     if (h && h->variant >= ST_PAPER_ORIGINAL)
         return set_error(ST_EUNSUPPORTED, "paper-literal variants cannot use the fused peer-store transport");
+    if (!h) return set_error(ST_EARG, "null handle");
     if (!drv().ok) return set_error(ST_EUNSUPPORTED, "driver stream memory operations unavailable");
+    int uva = 0, flush = 0;
+    cudaDeviceGetAttribute(&uva, cudaDevAttrUnifiedAddressing, h->device);
+    cudaDeviceGetAttribute(&flush, cudaDevAttrCanFlushRemoteWrites, h->device);
+    if (!uva) return set_error(ST_EUNSUPPORTED, "device %d has no unified addressing (CUDA IPC peer pointers)",
+                               h->device);
     DistState* d = nullptr;
     int rc = dist_attach_common(h, rank, nranks, &d);
     if (rc) return rc;
     d->p2p = new P2PState();
+    if (flush) d->p2p->wait_flags |= CU_STREAM_WAIT_VALUE_FLUSH;
     cudaError_t e = cudaMalloc(&d->p2p->flags, 256);
     if (e == cudaSuccess) e = cudaMemset(d->p2p->flags, 0, 256);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -316,7 +335,22 @@ static int open_rec(P2PState* p, const BlobRec& r, char** out) {
     if (it == p->opened.end()) {
         void* base = nullptr;
         cudaError_t e = cudaIpcOpenMemHandle(&base, r.handle, cudaIpcMemLazyEnablePeerAccess);
-        if (e != cudaSuccess) return set_error(ST_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+        if (e != cudaSuccess) {
+            cudaGetLastError();        // not sticky; clear it for the caller's fallback
+            return set_error(ST_EUNSUPPORTED, "cudaIpcOpenMemHandle: %s (no P2P path to the neighbour?)",
+                             cudaGetErrorString(e));
+        }
+        // the mapping lives on the neighbour's device: it must be reachable
+        // with peer loads / stores from this one (NVLink / NVSwitch)
+        cudaPointerAttributes pa;
+        int cur = -1, can = 1;
+        cudaGetDevice(&cur);
+        if (cudaPointerGetAttributes(&pa, base) == cudaSuccess && pa.device != cur && pa.device >= 0)
+            cudaDeviceCanAccessPeer(&can, cur, pa.device);
+        if (!can) {
+            cudaIpcCloseMemHandle(base);
+            return set_error(ST_EUNSUPPORTED, "device %d cannot access peer device %d", cur, pa.device);
+        }
         it = p->opened.emplace(key, (char*)base).first;
     }
     *out = it->second + r.offset;

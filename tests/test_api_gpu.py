@@ -122,3 +122,23 @@ def test_info_fields():
     assert i["interior_points"] == 62 * 16 * 12
     assert i["bytes_per_point"] == 24.0 and i["launches_per_step"] == 1
     assert i["lo"] == 2 and i["hi"] == 2 and i["nranks"] == 1
+
+
+def test_fusion_settings_validated():
+    """stencil_set_fusion: 0 auto, 1 off, 2 / 3 streaming (exactly that many
+    sweeps per launch), -S tile kernel; anything else ST_EARG; three
+    streaming sweeps of gaussblur ST_EUNSUPPORTED; info reports the depth."""
+    st = Stencil("jacobi2d5", (4100, 600), "f32")
+    for fu, spl in ((2, 2), (3, 3), (1, 1)):
+        st.set_fusion(fu)
+        assert st.info()["sweeps_per_launch"] == spl
+    for bad in (-1, 4, 65, -65):
+        with pytest.raises(StencilError) as e:
+            st.set_fusion(bad)
+        assert e.value.code == -1
+    g = Stencil("gaussblur5x5", (4100, 600), "f32")
+    with pytest.raises(StencilError) as e:
+        g.set_fusion(3)
+    assert e.value.code == -2
+    g.set_fusion(2)
+    assert g.info()["sweeps_per_launch"] == 2

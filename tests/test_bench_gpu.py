@@ -43,3 +43,29 @@ def test_slab_of_strong_share_attached():
     assert c["slab_of"] == 8 and c["parallelism"] == "slab1"
     assert c["dims"] == [1024, 1024, 128] and c["local_dims"] == [1024, 1024, 130]
     assert d["value"] > 0
+
+
+def test_gpus_flag_launches_ranks_itself():
+    """`python bench.py --gpus 2` without torchrun starts two ranks itself
+    (torch.distributed.run) and prints one line with n_gpus 2.  On a one-GPU
+    box both ranks share device 0 (STB200_BENCH_SHARE_GPU=1, gloo control
+    plane, p2p transport): a functional check of the launch, the slab
+    decomposition and the max-over-ranks timing, not a scaling number."""
+    env = dict(os.environ, STB200_BENCH_SHARE_GPU="1")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--workload",
+                        "jacobi3d", "--steps", "2", "--warmup", "3", "--no-e2e", "--no-cpu-baseline"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [l for l in p.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "slab2"
+    assert d["config"]["transport"] == "p2p" and d["config"]["dims"] == [1024, 1024, 2048]
+    assert d["value"] > 0
+
+
+def test_gpus_mismatch_rejected():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert p.returncode != 0 and "WORLD_SIZE" in p.stderr

@@ -334,6 +334,59 @@ def test_gradient_closed_form(oracle, dtype):
         assert np.all(o[1:-1, 1:-1, 1:-1] == v)
 
 
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_divergence_per_axis_coefficients(oracle, dtype):
+    """R9 with distinct per-axis coefficients (ax, ay, az) = (1/2, 1/4, 1/8):
+    (u, v, w) = (2i, -5j, 7k) has central differences (4, -10, 14), so
+    div = 2 - 2.5 + 1.75 = 1.25 exactly.  Any coefficient->axis permutation
+    gives another value (ax<->ay: 1 - 5 + 1.75 = -2.25; ax<->az: 0.5 - 2.5
+    + 7 = 5.0; ay<->az: 2 - 1.25 + 3.5 = 4.25), as does a coefficient applied
+    to the wrong array."""
+    npdt = np.float32 if dtype == "f32" else np.float64
+    shape = (6, 7, 12)
+    k, j, i = _ij(shape)
+    out = np.zeros(shape, npdt)
+    ins = [(2 * i).astype(npdt), (-5 * j).astype(npdt), (7 * k).astype(npdt)]
+    oracle.step("divergence", dtype, ins, [out], coeffs=[0.5, 0.25, 0.125])
+    assert np.all(out[1:-1, 1:-1, 1:-1] == 1.25)
+    oracle.step("divergence", dtype, ins, [out], coeffs=[0.25, 0.5, 0.125])
+    assert np.all(out[1:-1, 1:-1, 1:-1] == -2.25)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_gradient_per_axis_coefficients(oracle, dtype):
+    """R10 with (ax, ay, az) = (1/2, 1/4, 1/8): u = 3i - 2j + 5k has central
+    differences (6, -4, 10), so (gx, gy, gz) = (3, -1, 1.25) exactly; each
+    output carries its own axis' coefficient."""
+    npdt = np.float32 if dtype == "f32" else np.float64
+    shape = (6, 7, 12)
+    k, j, i = _ij(shape)
+    u = (3 * i - 2 * j + 5 * k).astype(npdt)
+    outs = [np.zeros_like(u) for _ in range(3)]
+    oracle.step("gradient", dtype, [u], outs, coeffs=[0.5, 0.25, 0.125])
+    for o, v in zip(outs, (3.0, -1.0, 1.25)):
+        assert np.all(o[1:-1, 1:-1, 1:-1] == v)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_jacobi_centre_coefficient(oracle, dtype):
+    """A non-zero centre weight (the default jacobi2d5 / jacobi3d7 centre
+    weight is 0): with (c0, c1) = (1/2, 1/8), i^2+j^2 -> (1/2 + 4/8) f +
+    (1/8)*4 = f + 1/2; in 3-D with (a, b) = (1/4, 1/8), i^2+j^2+k^2 ->
+    (1/4 + 6/8) f + (1/8)*6 = f + 3/4.  Exact (dyadic)."""
+    npdt = np.float32 if dtype == "f32" else np.float64
+    j, i = _ij((19, 24))
+    f = (i * i + j * j).astype(npdt)
+    out = np.zeros_like(f)
+    oracle.step("jacobi2d5", dtype, [f], [out], coeffs=[0.5, 0.125])
+    np.testing.assert_array_equal(out[1:-1, 1:-1], f[1:-1, 1:-1] + 0.5)
+    k, j, i = _ij((7, 9, 12))
+    f = (i * i + j * j + k * k).astype(npdt)
+    out = np.zeros_like(f)
+    oracle.step("jacobi3d7", dtype, [f], [out], coeffs=[0.25, 0.125])
+    np.testing.assert_array_equal(out[1:-1, 1:-1, 1:-1], f[1:-1, 1:-1, 1:-1] + 0.75)
+
+
 def _tri_inputs(shape, X, Y, Z, f):
     return [f, np.full(shape, X) if np.isscalar(X) else X,
             np.full(shape, Y) if np.isscalar(Y) else Y,

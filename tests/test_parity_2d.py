@@ -77,13 +77,17 @@ def test_run_parity(oracle, kind, dtype, shape):
     ("jacobi2d5", "f32", (61, 132)), ("jacobi2d9", "f64", (45, 130)),
     ("gaussblur5x5", "f32", (77, 1028)), ("gaussblur5x5", "f64", (33, 258)),
     ("gameoflife", "i32", (130, 260)), ("jacobi2d5", "f32", (3, 4))])
-@pytest.mark.parametrize("fusion,n", [(0, 7), (2, 7), (2, 10), (2, 1), (3, 10), (16, 11), (4, 1)])
+@pytest.mark.parametrize("fusion,n", [(0, 7), (2, 7), (2, 10), (2, 1), (3, 10), (3, 8), (-3, 10),
+                                      (-16, 11), (-4, 1)])
 def test_fused_runs_bit_identical(oracle, kind, dtype, shape, fusion, n):
-    """Temporal blocking (stencil_set_fusion: 2 = streaming two-sweep kernel,
-    >= 3 = shared-memory tile kernel, 0 = auto): the reported result buffer
-    holds the same bits as single sweeps, and oracle parity."""
+    """Temporal blocking (stencil_set_fusion: 2 / 3 = streaming kernel with
+    two / three sweeps per launch, -S = shared-memory tile kernel, 0 =
+    auto): the reported result buffer holds the same bits as single sweeps,
+    and oracle parity."""
     import torch
     from paper_2301_11389_b200.binding import Stencil
+    if fusion == 3 and kind == "gaussblur5x5":
+        pytest.skip("no three-sweep gaussblur kernel (ST_EUNSUPPORTED, tested in test_api_gpu)")
     f = inputs.generate_np(shape, dtype, inputs.BASE_SEED + 8)
     bufs = [f.copy(), np.zeros_like(f)]
     ridx = oracle.run(kind, dtype, bufs, n)

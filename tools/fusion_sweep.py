@@ -18,7 +18,7 @@ CASES = [c for c in CASES if not os.environ.get("KINDS") or c[0] + ":" + c[1] in
 for kind, dt, n, iters in CASES:
     a = inputs.generate_torch((n, n), dt, inputs.BASE_SEED + 1)
     b = torch.zeros_like(a)
-    for fusion in [int(x) for x in os.environ.get("DEPTHS", "1,2,3,4,6,8").split(",")]:
+    for fusion in [int(x) for x in os.environ.get("DEPTHS", "1,2,3,-4,-6,-8").split(",")]:
         st = Stencil(kind, (n, n), dt, variant=os.environ.get("VARIANT", "shuffle"))
         st.set_fusion(fusion)
         for _ in range(2):
