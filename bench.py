@@ -54,9 +54,11 @@ WORKLOADS = {
                      config="BASELINE configs[2]: wave13pt 3D 13-point fp64 512^3"),
     "tricubic": dict(kind="tricubic", dtype="f32", dims=(256, 256, 256), iters=10,
                      config="BASELINE configs[3]: tricubic 3D fp32 256^3",
-                     # FP32 flops per point of the factored form:
-                     # sums 21 mul + 63 fma, weights 9 mul + 15 fma -> 30 + 2*78
-                     flops_per_point=186),
+                     # FMA-pipe lane operations per point of the factored form
+                     # (DESIGN.md §5.3): 84 for the sums (64 x + 16 y + 4 z), 24
+                     # for the Lagrange weights (8 per axis); one lane-op per
+                     # FMUL / FFMA lane, two per FMUL2 / FFMA2 lane
+                     lane_ops_per_point=108),
     "jacobi3d": dict(kind="jacobi3d7", dtype="f32", dims=(1024, 1024, 1024), iters=10,
                      config="BASELINE configs[4]: jacobi 3D 7-point fp32 1024^2 x (1024*N)"),
     "divergence": dict(kind="divergence", dtype="f32", dims=(512, 512, 512), iters=10,
@@ -618,19 +620,28 @@ def main():
                                                        (1 if n_bufs == 2 else 0))),
             "cpu_baseline": cpu,
         }
-        if wl.get("flops_per_point"):
-            # the FP32 side of the roofline (the HBM side is the tighter one on
-            # paper: 20 B/pt against 186 flop/pt): nominal 128 FP32 lanes x 2
-            # flop per SM per clock at clocks.max.sm
+        if wl.get("lane_ops_per_point"):
+            # the FP32 side of the roofline: FMA-pipe lane
+            # operations per point against (a) the nominal 128 FP32 lanes per SM
+            # per clock and (b) the measured FFMA2 rate, 109 lanes/clk/SM
+            # (profiles/r01_microbench.json), both at clocks.max.sm
             mhz = 1965.0
             mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
             if os.path.exists(mp):
                 mhz = float(json.load(open(mp)).get("sm_max_mhz", mhz))
-            fpeak = sm_count() * 128 * 2 * mhz * 1e6 / 1e12
-            fach = wl["flops_per_point"] * pts_rank / avg_launch_s / 1e12
-            line["roofline"]["alu"] = {"achieved": fach, "peak": fpeak, "unit": "TFLOP/s", "frac": fach / fpeak,
-                                       "flops_per_point": wl["flops_per_point"],
-                                       "peak_source": "148 SMs x 128 FP32 lanes x 2 flop x clocks.max.sm"}
+            ops = wl["lane_ops_per_point"]
+            ach = ops * pts_rank / avg_launch_s / 1e12
+            nominal = sm_count() * 128 * mhz * 1e6 / 1e12
+            ffma2 = sm_count() * 109 * mhz * 1e6 / 1e12
+            line["roofline"]["alu"] = {
+                "achieved": ach, "unit": "T lane-ops/s", "lane_ops_per_point": ops,
+                "peak": nominal, "frac": ach / nominal,
+                "peak_source": "148 SMs x 128 FP32 lanes x clocks.max.sm",
+                "peak_ffma2": ffma2, "frac_ffma2": ach / ffma2,
+                "peak_ffma2_source": "148 SMs x 109 lanes/clk (measured FFMA2 rate, profiles/r01_microbench.json)",
+                "ceiling_gpts": {"hbm": peak * 1e9 / info["bytes_per_point"] / 1e9,
+                                 "fp32_nominal": nominal * 1e12 / ops / 1e9,
+                                 "fp32_ffma2": ffma2 * 1e12 / ops / 1e9}}
         print(json.dumps(line), flush=True)
     st.close()
     if world > 1:

@@ -312,6 +312,8 @@ static cudaError_t launch_tri2(const stencil_s* h, const void* const* in, void* 
 
 cudaError_t launch_tricubic(const stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
                             int64_t a, int64_t b) {
+    // fp32: ktricubic2 (default); STB200_TRI1=1 selects the one-row
+    // ktricubic (A/B experiments)
     static const int old1 = getenv("STB200_TRI1") ? atoi(getenv("STB200_TRI1")) : 0;
     if (h->dtype == ST_F32 && !old1)
         return h->variant == ST_PLAIN ? launch_tri2<1>(h, in, out, s, a, b) : launch_tri2<0>(h, in, out, s, a, b);
