@@ -72,6 +72,11 @@ static const kind_t KINDS[] = {
     {"divergence",      3, 3, 1, 1, 1, 3, 0, 1, 0},
     {"gradient",        3, 1, 3, 1, 1, 3, 0, 1, 0},
     {"tricubic",        3, 4, 1, 1, 2, 0, 0, 1, 0},
+    /* SURVEY §8(f) row f3 (DESIGN.md §3 readings R19-R22) */
+    {"tricubic2",       3, 4, 1, 1, 2, 0, 0, 1, 0},
+    {"uxx1",            3, 5, 1, 2, 1, 3, 0, 1, 0},
+    {"lapgsrb",         3, 1, 1, 1, 1, 1, 1, 1, 0},
+    {"whispering",      2, 8, 3, 1, 1, 0, 0, 1, 0},
 };
 
 static const kind_t* find_kind(const char* name) {
@@ -119,6 +124,12 @@ int oracle_default_coeffs(const char* kind, double* out, int cap) {
         out[0] = 2.0 - 7.5 * lam; out[1] = 4.0 * lam / 3.0; out[2] = -lam / 12.0;
     }
     else if (!strcmp(n, "divergence") || !strcmp(n, "gradient")) { out[0] = out[1] = out[2] = 0.5; }
+    else if (!strcmp(n, "uxx1")) {
+        /* (dth, c1, c2): dth = dt/h (R20: a value of the reading), c1 = 9/8,
+         * c2 = -1/24 the 4th-order staggered-grid difference weights */
+        out[0] = 0.25; out[1] = 9.0 / 8.0; out[2] = -1.0 / 24.0;
+    }
+    else if (!strcmp(n, "lapgsrb")) { out[0] = 1.0 / 6.0; }   /* Gauss-Seidel weight of the 7-point Laplace operator */
     return k->ncoeffs;
 }
 
@@ -273,6 +284,125 @@ static double pt_tricubic(const geom_t* g, const void* f, const void* X, const v
     return sc;
 }
 
+/* tricubic2 — Table 1 "tricubic2 ... 48 / 67", the same
+ * 64 + 3 loads and the same 48 shuffles as tricubic.  Reading R19: the same
+ * interpolation (cubic Lagrange on nodes {-1,0,1,2}, R11) written as the
+ * fully expanded 64-term sum, each term's weight the product of its three
+ * 1-D weights:
+ *   g = sum_c sum_b sum_a ((wx[a]*wy[b])*wz[c]) * f[k+c-1][j+b-1][i+a-1]
+ * one running sum, c outer, a inner, starting from the first product.     */
+static double pt_tricubic2(const geom_t* g, const void* f, const void* X, const void* Y,
+                           const void* Z, int64_t k, int64_t j, int64_t i) {
+    const int dt = g->dt;
+    double wx[4], wy[4], wz[4];
+    lagrange4(rd(X, dt, I3(g, k, j, i)), wx);
+    lagrange4(rd(Y, dt, I3(g, k, j, i)), wy);
+    lagrange4(rd(Z, dt, I3(g, k, j, i)), wz);
+    double s = 0.0;
+    for (int c = 0; c < 4; ++c)
+        for (int b = 0; b < 4; ++b)
+            for (int a = 0; a < 4; ++a) {
+                const double t = ((wx[a] * wy[b]) * wz[c]) * rd(f, dt, I3(g, k + c - 1, j + b - 1, i + a - 1));
+                s = (a == 0 && b == 0 && c == 0) ? t : s + t;
+            }
+    return s;
+}
+
+/* uxx1 — Table 1 "uxx1 ... 3 / 17, delta 2.00" (512x512x1024,
+ * PAPER.md:645-646).  Reading R20: the velocity update u1 of a 4th-order
+ * staggered-grid elastic wave code, one output from five arrays
+ * (u1, d1, xx, xy, xz), lo = 2, hi = 1 per axis:
+ *   d   = 0.25*(d1[k][j][i] + d1[k][j-1][i] + d1[k-1][j][i] + d1[k-1][j-1][i])
+ *   out = u1[k][j][i] + (dth/d) * ( c1*(xx[i]-xx[i-1] + xy[j]-xy[j-1] + xz[k]-xz[k-1])
+ *                                 + c2*(xx[i+1]-xx[i-2] + xy[j+1]-xy[j-2] + xz[k+1]-xz[k-2]) )
+ * (xx taps along x, xy along y, xz along z, at the point otherwise).
+ * Loads: u1 1 + d1 4 + xx 4 + xy 4 + xz 4 = 17; only xx's four taps share
+ * an x-row: 3 shuffles of delta 1, 2, 3 from the x-end (R1): 2.00.        */
+static double pt_uxx1(const geom_t* g, const void* const* in, const double* c,
+                      int64_t k, int64_t j, int64_t i) {
+    const int dt = g->dt;
+    const void *u1 = in[0], *d1 = in[1], *xx = in[2], *xy = in[3], *xz = in[4];
+    const double d = 0.25 * (rd(d1, dt, I3(g, k, j, i)) + rd(d1, dt, I3(g, k, j - 1, i))
+                             + rd(d1, dt, I3(g, k - 1, j, i)) + rd(d1, dt, I3(g, k - 1, j - 1, i)));
+    const double s1 = rd(xx, dt, I3(g, k, j, i)) - rd(xx, dt, I3(g, k, j, i - 1))
+                    + rd(xy, dt, I3(g, k, j, i)) - rd(xy, dt, I3(g, k, j - 1, i))
+                    + rd(xz, dt, I3(g, k, j, i)) - rd(xz, dt, I3(g, k - 1, j, i));
+    const double s2 = rd(xx, dt, I3(g, k, j, i + 1)) - rd(xx, dt, I3(g, k, j, i - 2))
+                    + rd(xy, dt, I3(g, k, j + 1, i)) - rd(xy, dt, I3(g, k, j - 2, i))
+                    + rd(xz, dt, I3(g, k + 1, j, i)) - rd(xz, dt, I3(g, k - 2, j, i));
+    return rd(u1, dt, I3(g, k, j, i)) + (c[0] / d) * (c[1] * s1 + c[2] * s2);
+}
+
+/* lapgsrb — Table 1 "lapgsrb ... 12 / 25, delta 1.83", the
+ * red-black Gauss-Seidel smoother of the 3-D Laplace operator ("lap" +
+ * "gsrb").  Reading R21: one full red-black iteration (red half-sweep, then
+ * black half-sweep reading the new red values) as one out-of-place
+ * point-wise pass, w the Gauss-Seidel weight (1/6 by default):
+ *   red(p)  = (i+j+k) even
+ *   nb6(q)  = u[q-x] + u[q+x] + u[q-y] + u[q+y] + u[q-z] + u[q+z]   (that order)
+ *   r(q)    = w*nb6(q) if q is an interior red point, else u[q]  (the boundary ring is held)
+ *   out(p)  = red(p) ? r(p) : w*(r(p-x) + r(p+x) + r(p-y) + r(p+y) + r(p-z) + r(p+z))
+ * A black point's six neighbours are red; each new red value is recomputed
+ * from the old field, so the loads of one point are the 25 points at L1
+ * distance <= 2 (6 for a red point, 19 for a black one; the lanes of a warp
+ * alternate between the two branches: divergent).  Their x-rows give 12
+ * shuffles of total delta 22 from the x-end (R1): 1.83.  The boundary ring
+ * is 1 wide: reads stay inside the grid because r of a ring point is u.   */
+static int lap_interior(const geom_t* g, int64_t k, int64_t j, int64_t i) {
+    return i >= 1 && i < g->nx - 1 && j >= 1 && j < g->ny - 1 && k >= 1 && k < g->nz - 1;
+}
+static double lap_nb6(const geom_t* g, const void* u, int64_t k, int64_t j, int64_t i) {
+    const int dt = g->dt;
+    return rd(u, dt, I3(g, k, j, i - 1)) + rd(u, dt, I3(g, k, j, i + 1))
+         + rd(u, dt, I3(g, k, j - 1, i)) + rd(u, dt, I3(g, k, j + 1, i))
+         + rd(u, dt, I3(g, k - 1, j, i)) + rd(u, dt, I3(g, k + 1, j, i));
+}
+static double lap_red(const geom_t* g, const void* u, double w, int64_t k, int64_t j, int64_t i) {
+    if (lap_interior(g, k, j, i) && ((i + j + k) & 1) == 0) return w * lap_nb6(g, u, k, j, i);
+    return rd(u, g->dt, I3(g, k, j, i));
+}
+static double pt_lapgsrb(const geom_t* g, const void* u, const double* c,
+                         int64_t k, int64_t j, int64_t i) {
+    const double w = c[0];
+    if (((i + j + k) & 1) == 0) return lap_red(g, u, w, k, j, i);
+    return w * (lap_red(g, u, w, k, j, i - 1) + lap_red(g, u, w, k, j, i + 1)
+                + lap_red(g, u, w, k, j - 1, i) + lap_red(g, u, w, k, j + 1, i)
+                + lap_red(g, u, w, k - 1, j, i) + lap_red(g, u, w, k + 1, j, i));
+}
+
+/* whispering — Table 1 "whispering ... 6 / 19, delta 0.83" (
+ * 2-D, "more buffers are allocated", 8192x16384).
+ * Reading R22: one leapfrog step of the 2-D TM-mode Yee scheme (FDTD) of a
+ * whispering-gallery resonator — per-cell material arrays carry the
+ * dielectric (cb) and the absorbing layer (dax, dbx, day, dby) — with the
+ * magnetic half step fused into the electric one: the two neighbouring H
+ * values the Ez update needs are recomputed from the old fields.
+ * in = (Hx, Hy, Ez, dax, dbx, day, dby, cb), out = (Hx', Hy', Ez'):
+ *   hx(q) = dax[q]*Hx[q] - dbx[q]*(Ez[q+y] - Ez[q])
+ *   hy(q) = day[q]*Hy[q] + dby[q]*(Ez[q+x] - Ez[q])
+ *   Hx'(p) = hx(p);  Hy'(p) = hy(p)
+ *   Ez'(p) = Ez[p] + cb[p]*((hy(p) - hy(p-x)) - (hx(p) - hx(p-y)))
+ * 18 distinct taps; Ez[p] is loaded again for Ez' after the stores of Hx'
+ * and Hy' (the N=0 reuse): 19 loads, 6 shuffles of total delta 5.        */
+static double wh_hx(const geom_t* g, const void* const* in, int64_t j, int64_t i) {
+    const int dt = g->dt;
+    return rd(in[3], dt, I2(g, j, i)) * rd(in[0], dt, I2(g, j, i))
+         - rd(in[4], dt, I2(g, j, i)) * (rd(in[2], dt, I2(g, j + 1, i)) - rd(in[2], dt, I2(g, j, i)));
+}
+static double wh_hy(const geom_t* g, const void* const* in, int64_t j, int64_t i) {
+    const int dt = g->dt;
+    return rd(in[5], dt, I2(g, j, i)) * rd(in[1], dt, I2(g, j, i))
+         + rd(in[6], dt, I2(g, j, i)) * (rd(in[2], dt, I2(g, j, i + 1)) - rd(in[2], dt, I2(g, j, i)));
+}
+static void pt_whispering(const geom_t* g, const void* const* in, int64_t j, int64_t i,
+                          double* hx, double* hy, double* ez) {
+    const int dt = g->dt;
+    *hx = wh_hx(g, in, j, i);
+    *hy = wh_hy(g, in, j, i);
+    *ez = rd(in[2], dt, I2(g, j, i))
+        + rd(in[7], dt, I2(g, j, i)) * ((*hy - wh_hy(g, in, j, i - 1)) - (*hx - wh_hx(g, in, j - 1, i)));
+}
+
 /* ------------------------------------------------------------- driver */
 static int check(const kind_t* k, int dt, int ndims, const int64_t* dims, int ncoeffs) {
     if (!k) return fail("unknown kind");
@@ -310,7 +440,14 @@ int oracle_step(const char* kind, const char* dtype, int ndims, const int64_t* d
                 case 0: wr(out[0], dt, o, pt_jacobi2d5(&g, in[0], c, j, i)); break;
                 case 1: wr(out[0], dt, o, pt_jacobi2d9(&g, in[0], c, j, i)); break;
                 case 2: wr(out[0], dt, o, pt_gaussblur(&g, in[0], c, j, i)); break;
-                default: ((int32_t*)out[0])[o] = pt_gameoflife(&g, (const int32_t*)in[0], j, i);
+                case 3: ((int32_t*)out[0])[o] = pt_gameoflife(&g, (const int32_t*)in[0], j, i); break;
+                default: {          /* whispering: out = (Hx', Hy', Ez') */
+                    double hx, hy, ez;
+                    pt_whispering(&g, in, j, i, &hx, &hy, &ez);
+                    wr(out[0], dt, o, hx);
+                    wr(out[1], dt, o, hy);
+                    wr(out[2], dt, o, ez);
+                }
                 }
             }
         return 0;
@@ -335,8 +472,14 @@ int oracle_step(const char* kind, const char* dtype, int ndims, const int64_t* d
                     wr(out[2], dt, o, gz);
                     break;
                 }
-                default:             /* tricubic: in = (f, X, Y, Z) */
-                    wr(out[0], dt, o, pt_tricubic(&g, in[0], in[1], in[2], in[3], kk, j, i));
+                case 9:              /* tricubic: in = (f, X, Y, Z) */
+                    wr(out[0], dt, o, pt_tricubic(&g, in[0], in[1], in[2], in[3], kk, j, i)); break;
+                case 10:             /* tricubic2: the expanded 64-term form */
+                    wr(out[0], dt, o, pt_tricubic2(&g, in[0], in[1], in[2], in[3], kk, j, i)); break;
+                case 11:             /* uxx1: in = (u1, d1, xx, xy, xz) */
+                    wr(out[0], dt, o, pt_uxx1(&g, in, c, kk, j, i)); break;
+                default:             /* lapgsrb */
+                    wr(out[0], dt, o, pt_lapgsrb(&g, in[0], c, kk, j, i));
                 }
             }
     return 0;
@@ -392,8 +535,8 @@ int oracle_run(const char* kind, const char* dtype, int ndims, const int64_t* di
         if (result_idx) *result_idx = c;
         return 0;
     }
-    /* divergence / gradient / tricubic: re-apply the same step */
-    const void* in[4];
+    /* divergence / gradient / tricubic / tricubic2 / uxx1 / whispering: re-apply the same step */
+    const void* in[8];
     void* out[3];
     for (int a = 0; a < k->n_in; ++a) in[a] = bufs[a];
     for (int a = 0; a < k->n_out; ++a) out[a] = bufs[k->n_in + a];

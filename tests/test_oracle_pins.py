@@ -16,7 +16,8 @@ import scipy.ndimage as ndi
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 ALL_KINDS = ["jacobi2d5", "jacobi2d9", "gaussblur5x5", "gameoflife", "laplacian3d7",
-             "jacobi3d7", "wave13pt", "divergence", "gradient", "tricubic"]
+             "jacobi3d7", "wave13pt", "divergence", "gradient", "tricubic",
+             "tricubic2", "uxx1", "lapgsrb", "whispering"]
 
 
 def read_sections(path):
@@ -43,15 +44,23 @@ def interior(kind_ar, shape):
 
 
 # --------------------------------------------------------------- Table 1
-def _dependencies(oracle, kind, seed=1):
-    """Brute force: which (array, offset) inputs change the output at a point."""
+def _dependencies(oracle, kind, seed=1, centres=None):
+    """Brute force: which (array, offset) inputs change the output at a point
+    (the union over `centres`: lapgsrb's red and black points take different
+    branches)."""
     ar = oracle.arity(kind)
     nd = ar["ndims"]
     n = 11
     shape = (n,) * nd
     dtype = "i32" if kind == "gameoflife" else "f64"
     rng = np.random.default_rng(seed)
-    centre = (n // 2,) * nd
+    deps = set()
+    for centre in centres or [(n // 2,) * nd]:
+        deps |= _deps_at(oracle, kind, ar, nd, shape, dtype, rng, centre)
+    return deps
+
+
+def _deps_at(oracle, kind, ar, nd, shape, dtype, rng, centre):
     deps = set()
     trials = 40 if kind == "gameoflife" else 2
     for _ in range(trials):
@@ -76,6 +85,22 @@ def _dependencies(oracle, kind, seed=1):
                 if any(o2[centre] != b for o2, b in zip(outs2, base)):
                     deps.add((a, off[::-1]))        # store offset as (dx, dy[, dz])
     return deps
+
+
+def _table1_counts_ordered(loads):
+    """The paper's selection rule on a load sequence in program order: loads
+    of one array that differ only along x share a source, the first of them
+    in program order; every later one is a shuffle of delta |x - x_source|
+    (a shuffled load is never a source)."""
+    src, shuffles, delta_sum = {}, 0, 0
+    for a, off in loads:
+        key = (a, off[1:])
+        if key not in src:
+            src[key] = off[0]
+        else:
+            shuffles += 1
+            delta_sum += abs(off[0] - src[key])
+    return shuffles, len(loads), (delta_sum / shuffles if shuffles else 0.0)
 
 
 def _table1_counts(deps):
@@ -108,7 +133,19 @@ def test_table1_load_and_shuffle_counts(oracle, row):
     """Table 1: loads, shuffles and average delta follow
     from the tap set of each stencil — pins radius, tap set and arity."""
     _, kind, shuffles, loads, delta = row
-    s, l, d = _table1_counts(_dependencies(oracle, kind))
+    if kind == "lapgsrb":                  # union of a black (5,5,5) and a red (6,5,5) point
+        deps = _dependencies(oracle, kind, centres=[(5, 5, 5), (5, 5, 6)])
+        assert len(deps) == 25 and all(sum(map(abs, o)) <= 2 for _, o in deps)   # the L1 ball
+    else:
+        deps = _dependencies(oracle, kind)
+    if kind == "whispering":
+        seq = [(int(r[0]), (int(r[1]), int(r[2])))
+               for r in (l.split() for l in open(os.path.join(GOLDEN, "whispering_loads.txt")))
+               if r and not r[0].startswith("#")]
+        assert set(seq) == deps            # the reading's load sequence covers exactly the oracle's taps
+        s, l, d = _table1_counts_ordered(seq)
+    else:
+        s, l, d = _table1_counts(deps)
     assert (s, l) == (shuffles, loads)
     assert abs(d - delta) < 0.005
 
