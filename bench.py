@@ -65,6 +65,15 @@ WORKLOADS = {
                        config="divergence fp32 512^3 (suite member, Table 1)"),
     "gradient": dict(kind="gradient", dtype="f32", dims=(512, 512, 512), iters=10,
                      config="gradient fp32 512^3 (suite member, Table 1)"),
+    # SURVEY §8(f) row f3 at the paper's problem sizes
+    "uxx1": dict(kind="uxx1", dtype="f32", dims=(512, 512, 1024), iters=10,
+                 config="uxx1 fp32 512x512x1024 (suite member, Table 1; paper size)"),
+    "whispering": dict(kind="whispering", dtype="f32", dims=(8192, 16384), iters=10,
+                       config="whispering fp32 8192x16384 (suite member, Table 1; paper size)"),
+    "lapgsrb": dict(kind="lapgsrb", dtype="f32", dims=(512, 1024, 1024), iters=10,
+                    config="lapgsrb fp32 512x1024x1024 (suite member, Table 1; paper 3-D size)"),
+    "tricubic2": dict(kind="tricubic2", dtype="f32", dims=(256, 256, 256), iters=10,
+                      config="tricubic2 fp32 256^3 (suite member, Table 1)", lane_ops_per_point=108),
 }
 L2_BYTES = 126 * 2**20
 METRIC = "Gpoints/s and achieved HBM GB/s (% of ~8 TB/s) per stencil, 1/2/4/8 B200"

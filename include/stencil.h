@@ -56,11 +56,24 @@ typedef struct stencil_s* stencil_t;
  *  ST_DIVERGENCE    (u,v,w) -> out, r=1      Table 1 divergence         coeffs (ax,ay,az)    default (1/2,1/2,1/2)
  *  ST_GRADIENT      u -> (gx,gy,gz), r=1     Table 1 gradient           coeffs (ax,ay,az)    default (1/2,1/2,1/2)
  *  ST_TRICUBIC      (f,X,Y,Z) -> g, lo=1 hi=2  Table 1 tricubic, 67 loads none
+ * SURVEY §8(f) row f3 (readings DESIGN.md §3 R19-R22; PAPER.md prints no formula):
+ *  ST_TRICUBIC2     (f,X,Y,Z) -> g, lo=1 hi=2  Table 1 tricubic2: tricubic as the
+ *                   expanded 64-term sum; the same function up to rounding   none
+ *  ST_UXX1          (u1,d1,xx,xy,xz) -> u1', lo=2 hi=1  Table 1 uxx1: 4th-order
+ *                   staggered velocity update, 17 loads             coeffs (dth,c1,c2)   default (1/4, 9/8, -1/24)
+ *  ST_LAPGSRB       u -> u', r=1  Table 1 lapgsrb: one red-black Gauss-Seidel
+ *                   iteration of the 7-point Laplace operator, 25 loads (L1 ball of radius 2)
+ *                                                                   coeffs (w)           default 1/6
+ *  ST_WHISPERING    (Hx,Hy,Ez,dax,dbx,day,dby,cb) -> (Hx',Hy',Ez'), 2-D, r=1  Table 1 whispering
+ *                   (PAPER.md:608): one fused TM-mode Yee (FDTD) leapfrog step, 19 loads   none
+ * The f3 kinds run on one GPU (stencil_dist_attach*: ST_EUNSUPPORTED) with the
+ * SHUFFLE / PLAIN variants (paper-literal variants: ST_EUNSUPPORTED).
  * Formulas: DESIGN.md §3 (and oracle/oracle.c, the independent CPU oracle). */
 enum stencil_kind {
     ST_JACOBI2D5 = 1, ST_JACOBI2D9 = 2, ST_GAUSSBLUR5X5 = 3, ST_GAMEOFLIFE = 4,
     ST_LAPLACIAN3D7 = 5, ST_JACOBI3D7 = 6, ST_WAVE13PT = 7, ST_DIVERGENCE = 8,
-    ST_GRADIENT = 9, ST_TRICUBIC = 10
+    ST_GRADIENT = 9, ST_TRICUBIC = 10,
+    ST_TRICUBIC2 = 11, ST_UXX1 = 12, ST_LAPGSRB = 13, ST_WHISPERING = 14
 };
 
 /* Element types.  ST_I32 only for ST_GAMEOFLIFE; the others take F32/F64. */

@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("STB200_LIB") or os.path.join(PKG, "libstencil_b200.so
 
 KINDS = {"jacobi2d5": 1, "jacobi2d9": 2, "gaussblur5x5": 3, "gameoflife": 4,
          "laplacian3d7": 5, "jacobi3d7": 6, "wave13pt": 7, "divergence": 8,
-         "gradient": 9, "tricubic": 10}
+         "gradient": 9, "tricubic": 10, "tricubic2": 11, "uxx1": 12, "lapgsrb": 13, "whispering": 14}
 DTYPES = {"f32": 1, "f64": 2, "i32": 3}
 VARIANTS = {"shuffle": 0, "plain": 1, "paper_original": 2, "paper_ptxasw": 3,
             "paper_noload": 4, "paper_nocorner": 5, "paper_uniform": 6}

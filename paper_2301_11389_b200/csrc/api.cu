@@ -47,6 +47,10 @@ const KindInfo* stb200::kind_info(int kind) {
         {ST_DIVERGENCE, "divergence", 3, 3, 1, 1, 1, 3, 0, true, false},
         {ST_GRADIENT, "gradient", 3, 1, 3, 1, 1, 3, 0, true, false},
         {ST_TRICUBIC, "tricubic", 3, 4, 1, 1, 2, 0, 0, true, false},
+        {ST_TRICUBIC2, "tricubic2", 3, 4, 1, 1, 2, 0, 0, true, false},
+        {ST_UXX1, "uxx1", 3, 5, 1, 2, 1, 3, 0, true, false},
+        {ST_LAPGSRB, "lapgsrb", 3, 1, 1, 1, 1, 1, 1, true, false},
+        {ST_WHISPERING, "whispering", 2, 8, 3, 1, 1, 0, 0, true, false},
     };
     for (const auto& k : table)
         if (k.kind == kind) return &k;
@@ -75,6 +79,8 @@ static void default_coeffs(int kind, double* c) {
     }
     case ST_DIVERGENCE:
     case ST_GRADIENT: c[0] = c[1] = c[2] = 0.5; break;
+    case ST_UXX1: c[0] = 0.25; c[1] = 9.0 / 8.0; c[2] = -1.0 / 24.0; break;   // dth, 4th-order stagger
+    case ST_LAPGSRB: c[0] = 1.0 / 6.0; break;                                  // Gauss-Seidel weight
     default: break;
     }
 }
@@ -146,6 +152,9 @@ extern "C" int stencil_set_variant(stencil_t h, int variant) {
     if (!h) return set_error(ST_EARG, "null handle");
     if (variant < ST_SHUFFLE || variant > ST_PAPER_UNIFORM)
         return set_error(ST_EUNSUPPORTED, "unknown variant %d", variant);
+    if (variant >= ST_PAPER_ORIGINAL && h->k->kind >= ST_TRICUBIC2)
+        return set_error(ST_EUNSUPPORTED, "no paper-literal variant for %s (SURVEY §8(f) f3 kinds: SHUFFLE / PLAIN)",
+                         h->k->name);
     if (variant >= ST_PAPER_ORIGINAL && h->dtype == ST_F64)
         return set_error(ST_EUNSUPPORTED,
                          "the paper-literal variants cover the fp32/int32 kinds (32-bit shuffles, "
@@ -456,7 +465,7 @@ static int enqueue_run(stencil_s* h, void* const* bufs, int n_iters, cudaStream_
         *result = c;
         return ST_OK;
     }
-    const void* in[4];
+    const void* in[8];
     void* out[3];
     for (int a = 0; a < k->n_in; ++a) in[a] = bufs[a];
     for (int b = 0; b < k->n_out; ++b) out[b] = bufs[k->n_in + b];

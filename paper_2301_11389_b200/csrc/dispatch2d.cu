@@ -101,6 +101,9 @@ static cudaError_t paper_var(const stencil_s* h, const void* in, void* out, cuda
     }
 }
 
+cudaError_t dispatch_f3(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s, int64_t a,
+                        int64_t b);
+
 cudaError_t dispatch_2d(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
                         int64_t a, int64_t b) {
     const bool f64 = h->dtype == ST_F64;
@@ -126,6 +129,7 @@ cudaError_t dispatch_2d(stencil_s* h, const void* const* in, void* const* out, c
     case ST_GAMEOFLIFE:
         if (h->variant == ST_PLAIN) return launch_k2d<OpLife, int, VAR_PLAIN>(h, in[0], out[0], s, a, b);
         return launch_k2d<OpLife, int, VAR_SHUFFLE>(h, in[0], out[0], s, a, b);
+    case ST_WHISPERING: return dispatch_f3(h, in, out, s, a, b);
     default: return cudaErrorInvalidValue;
     }
 }

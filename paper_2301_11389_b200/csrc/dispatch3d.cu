@@ -202,6 +202,9 @@ static cudaError_t paper3_var(const stencil_s* h, const void* const* in, void* c
     }
 }
 
+cudaError_t dispatch_f3(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s, int64_t a,
+                        int64_t b);
+
 cudaError_t dispatch_3d(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
                         int64_t a, int64_t b) {
     const bool f64 = h->dtype == ST_F64;
@@ -231,7 +234,10 @@ cudaError_t dispatch_3d(stencil_s* h, const void* const* in, void* const* out, c
         return f64 ? launch3_var<OpDivergence, double>(h, in, out, s, a, b)
                    : launch3_var<OpDivergence, float>(h, in, out, s, a, b);
     case ST_TRICUBIC:
+    case ST_TRICUBIC2:       // the same function up to rounding order (DESIGN.md §3 R19)
         return launch_tricubic(h, in, out, s, a, b);
+    case ST_UXX1:
+    case ST_LAPGSRB: return dispatch_f3(h, in, out, s, a, b);
     default: return cudaErrorInvalidValue;
     }
 }

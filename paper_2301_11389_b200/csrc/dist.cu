@@ -283,6 +283,9 @@ int dist_attach_common(stencil_t h, int rank, int nranks, DistState** out) {
     if (!h) return set_error(ST_EARG, "null handle");
     if (h->dist) return set_error(ST_ESTATE, "handle already attached");
     if (!h->graphs.empty()) return set_error(ST_ESTATE, "attach before the first run");
+    if (h->k->kind >= ST_TRICUBIC2)
+        return set_error(ST_EUNSUPPORTED, "%s runs on one GPU (SURVEY §8(f) f3 kind: no slab decomposition)",
+                         h->k->name);
     const int slow = h->ndims - 1;
     int64_t plan[8];
     int rc = stencil_slab_plan(h->dims[slow], h->k->lo, h->k->hi, rank, nranks, plan);

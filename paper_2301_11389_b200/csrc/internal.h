@@ -20,7 +20,7 @@ struct KindInfo {
 };
 
 struct GraphEntry {
-    void* bufs[8];
+    void* bufs[16];
     int nb, n_iters, variant, result;
     cudaGraphExec_t exec;
 };
