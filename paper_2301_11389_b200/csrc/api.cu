@@ -421,12 +421,10 @@ static int enqueue_run(stencil_s* h, void* const* bufs, int n_iters, cudaStream_
         }
         const int S = fusion_depth(h, n_iters);
         if (S > 1) {
-            // passes of <= S sweeps (the fused kernel also writes the ring
-            // cells, so no ring copy), an even/odd count matching n_iters so
-            // the result lands in bufs[n_iters % 2] exactly as with single
-            // sweeps (runs chain the same way)
-            int passes = (n_iters + S - 1) / S;
-            if ((passes & 1) != (n_iters & 1)) ++passes;
+            // as few passes of <= S sweeps as possible (one launch for a run
+            // of up to S sweeps; the fused kernels also write the ring cells,
+            // so no ring copy); the result buffer is reported in *result
+            const int passes = (n_iters + S - 1) / S;
             int cur = 0, done = 0;
             for (int p = 0; p < passes; ++p) {
                 const int sw = (n_iters - done) / (passes - p);     // even split, each >= 1

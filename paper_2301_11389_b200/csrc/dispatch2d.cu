@@ -5,6 +5,7 @@
 #include "k2d.cuh"
 #include "kpaper.cuh"
 #include "ktb2d.cuh"
+#include "ktb2r.cuh"
 #include "k2d2.cuh"
 
 namespace stb200 {
@@ -184,6 +185,34 @@ static cudaError_t launch_k2d2(const stencil_s* h, const void* in, void* out, cu
     return cudaGetLastError();
 }
 
+// All S sweeps of a small run in one launch, the field in registers (ktb2r.cuh).
+template <class Op, typename T, int VAR>
+static cudaError_t launch_tbr(const stencil_s* h, const void* in, void* out, cudaStream_t s, int S) {
+    constexpr int R = Op::R;
+    const int64_t nx = h->ldims[0], ny = h->ldims[1];
+    const int hh = S * R;
+    const int ow = tbr_width<T>() - 2 * hh - (kTbrV - 1), oh = kTbrWarps * kTbrRows - 2 * hh;
+    auto kern = ktb2r<Op, T, VAR>;
+    constexpr size_t smem = tbr_smem_bytes<T, R, VAR>();
+    kernel_setup((const void*)kern, h->device, smem, kTbrWarps * 32);
+    const dim3 grid((unsigned)((nx - 2 * R + ow - 1) / ow), (unsigned)((ny - 2 * R + oh - 1) / oh));
+    Coeffs<T, Op::NC> c{};
+    for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)h->coeffs[t];
+    kern<<<grid, kTbrWarps * 32, smem, s>>>((const T*)in, (T*)out, (int)nx, (int)ny, S, c);
+    return cudaGetLastError();
+}
+
+// S sweeps in one launch: the register kernel (ktb2r) when its region holds
+// the S*R halo, else the shared-memory tile kernel (ktb2d).
+template <class Op, typename T>
+static cudaError_t launch_fused(const stencil_s* h, const void* in, void* out, cudaStream_t s, int S) {
+    static const int env_old = getenv("STB200_TB_SMEM") ? atoi(getenv("STB200_TB_SMEM")) : 0;
+    if (!env_old && S <= tbr_max_sweeps<T>(Op::R))
+        return h->variant == ST_PLAIN ? launch_tbr<Op, T, VAR_PLAIN>(h, in, out, s, S)
+                                      : launch_tbr<Op, T, VAR_SHUFFLE>(h, in, out, s, S);
+    return launch_tb<Op, T>(h, in, out, s, S);
+}
+
 template <class Op, typename T>
 static cudaError_t pair_op(const stencil_s* h, const void* in, void* out, cudaStream_t s, int nsw) {
     if (h->variant == ST_PLAIN)
@@ -212,9 +241,12 @@ cudaError_t dispatch_2d_pair(stencil_s* h, const void* in, void* out, cudaStream
     }
 }
 
-// Largest fusion depth whose two shared-memory planes fit in ~100 KB.
+// Largest fusion depth: the register kernel's (ktb2r), or the shared-memory
+// tile kernel's (two planes in ~100 KB) when STB200_TB_SMEM selects it.
 int fused_max_sweeps(const stencil_s* h) {
     const int R = h->k->lo;
+    static const int env_old = getenv("STB200_TB_SMEM") ? atoi(getenv("STB200_TB_SMEM")) : 0;
+    if (!env_old) return h->dtype == ST_F64 ? tbr_max_sweeps<double>(R) : tbr_max_sweeps<float>(R);
     const size_t es = h->dtype == ST_F64 ? 8 : 4;
     int S = 16;
     while (S > 1 && 2 * (size_t)(kTbTileX + 2 * S * R) * (kTbTileY + 2 * S * R) * es > 100 * 1024) --S;
@@ -225,15 +257,15 @@ cudaError_t dispatch_2d_fused(stencil_s* h, const void* in, void* out, cudaStrea
     const bool f64 = h->dtype == ST_F64;
     switch (h->k->kind) {
     case ST_JACOBI2D5:
-        return f64 ? launch_tb<OpJacobi2D5<double>, double>(h, in, out, s, S)
-                   : launch_tb<OpJacobi2D5<float>, float>(h, in, out, s, S);
+        return f64 ? launch_fused<OpJacobi2D5<double>, double>(h, in, out, s, S)
+                   : launch_fused<OpJacobi2D5<float>, float>(h, in, out, s, S);
     case ST_JACOBI2D9:
-        return f64 ? launch_tb<OpJacobi2D9<double>, double>(h, in, out, s, S)
-                   : launch_tb<OpJacobi2D9<float>, float>(h, in, out, s, S);
+        return f64 ? launch_fused<OpJacobi2D9<double>, double>(h, in, out, s, S)
+                   : launch_fused<OpJacobi2D9<float>, float>(h, in, out, s, S);
     case ST_GAUSSBLUR5X5:
-        return f64 ? launch_tb<OpGauss5<double>, double>(h, in, out, s, S)
-                   : launch_tb<OpGauss5<float>, float>(h, in, out, s, S);
-    case ST_GAMEOFLIFE: return launch_tb<OpLife, int>(h, in, out, s, S);
+        return f64 ? launch_fused<OpGauss5<double>, double>(h, in, out, s, S)
+                   : launch_fused<OpGauss5<float>, float>(h, in, out, s, S);
+    case ST_GAMEOFLIFE: return launch_fused<OpLife, int>(h, in, out, s, S);
     default: return cudaErrorInvalidValue;
     }
 }
