@@ -12,6 +12,7 @@
 #include "ktricubic2.cuh"
 #include "kpaper3d.cuh"
 #include "kgrad.cuh"
+#include "klap2.cuh"
 
 namespace stb200 {
 
@@ -202,6 +203,45 @@ static cudaError_t paper3_var(const stencil_s* h, const void* const* in, void* c
     }
 }
 
+// lapgsrb (klap2.cuh): one-wave persistent grid, LockIter work order as k3d
+template <typename T, int VAR>
+static cudaError_t launch_lap2(const stencil_s* h, const void* const* in, void* const* out, cudaStream_t s,
+                               int64_t z_lo, int64_t z_hi) {
+    using L = LapLayout<T>;
+    auto kern = klapgsrb2<T, VAR>;
+    const int bps = kernel_setup((const void*)kern, h->device, L::SMEM, klap2_threads());
+    const int64_t* ld = h->ldims;
+    if (z_lo < 0) { z_lo = 1; z_hi = ld[2] - 1; }
+    if (z_hi <= z_lo) return cudaSuccess;
+    TmapPack<1> tm;
+    cudaError_t e = make_tmap(&tm.m[0], in[0], h->dtype, ld, L::BX, L::BY);
+    if (e != cudaSuccess) return e;
+    Lap2Args<T> args{};
+    args.out = (T*)out[0];
+    args.nx = ld[0];
+    args.ny = ld[1];
+    args.nz = ld[2];
+    args.z_lo = (int)z_lo;
+    args.nzo = (int)(z_hi - z_lo);
+    args.ntx = (int)((ld[0] + L::TX - 1) / L::TX);
+    args.nty = (int)((ld[1] + L::TY - 1) / L::TY);
+    const int64_t ncols = (int64_t)args.ntx * args.nty;
+    const int64_t slots = (int64_t)bps * sm_count_of(h->device);
+    int64_t zsplit = slots / ncols;
+    if (zsplit < 1) zsplit = 1;
+    if (zsplit > args.nzo) zsplit = args.nzo;
+    const int64_t items = ncols * zsplit;
+    const int64_t m = (items + slots - 1) / slots;
+    const int64_t grid = (items + m - 1) / m;
+    args.zsplit = (int)zsplit;
+    args.m = (int)m;
+    static const int zc_env = getenv("STB200_LAP_ZC") ? atoi(getenv("STB200_LAP_ZC")) : 0;
+    args.zc = zc_env > 0 ? zc_env : 64;
+    args.w = (T)h->coeffs[0];
+    kern<<<(unsigned)grid, klap2_threads(), L::SMEM, s>>>(tm, args);
+    return cudaGetLastError();
+}
+
 cudaError_t dispatch_f3(stencil_s* h, const void* const* in, void* const* out, cudaStream_t s, int64_t a,
                         int64_t b);
 
@@ -236,8 +276,17 @@ cudaError_t dispatch_3d(stencil_s* h, const void* const* in, void* const* out, c
     case ST_TRICUBIC:
     case ST_TRICUBIC2:       // the same function up to rounding order (DESIGN.md §3 R19)
         return launch_tricubic(h, in, out, s, a, b);
-    case ST_UXX1:
-    case ST_LAPGSRB: return dispatch_f3(h, in, out, s, a, b);
+    case ST_LAPGSRB: {
+        // klapgsrb2 (klap2.cuh, default); STB200_LAP1=1 selects the first
+        // z-marching kernel klapgsrb (kf3.cuh) for A/B experiments
+        static const int old1 = getenv("STB200_LAP1") ? atoi(getenv("STB200_LAP1")) : 0;
+        if (old1) return dispatch_f3(h, in, out, s, a, b);
+        if (f64) return h->variant == ST_PLAIN ? launch_lap2<double, 1>(h, in, out, s, a, b)
+                                               : launch_lap2<double, 0>(h, in, out, s, a, b);
+        return h->variant == ST_PLAIN ? launch_lap2<float, 1>(h, in, out, s, a, b)
+                                      : launch_lap2<float, 0>(h, in, out, s, a, b);
+    }
+    case ST_UXX1: return dispatch_f3(h, in, out, s, a, b);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -101,7 +101,8 @@ def _rank(rank, world, port, kind, dtype, dims, n_iters, q, transport="host", ru
         if transport == "p2p":
             st.p2p_register(bufs, _allgather)
         for _ in range(runs - 1):          # consecutive runs on the same buffers (epochs carry over)
-            st.run(bufs, n_iters)
+            i = st.run(bufs, n_iters)
+            assert i == n_iters % 2          # attached runs are single sweeps: no rotation needed
         idx = st.run(bufs, n_iters)
         torch.cuda.synchronize()
         nres = n_out if n_bufs > 3 else 1
@@ -117,7 +118,9 @@ def _rank(rank, world, port, kind, dtype, dims, n_iters, q, transport="host", ru
             else:
                 rb = [f.clone() for f in fields] + [torch.zeros_like(fields[0]) for _ in range(n_out)]
             for _ in range(runs - 1):
-                ref.run(rb, n_iters)
+                i = ref.run(rb, n_iters)
+                if n_bufs == 2 and i == 1:   # a fused 1-GPU run may end in bufs[1] (stencil.h)
+                    rb = [rb[1], rb[0]]
             ridx = ref.run(rb, n_iters)
             torch.cuda.synchronize()
             # the CPU oracle on the same global fields

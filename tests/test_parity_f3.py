@@ -27,6 +27,9 @@ SHAPES2 = {  # (ny, nx)
     "f32": [(3, 4), (5, 8), (29, 36), (70, 132), (41, 1028), (9, 2052)],
     "f64": [(3, 4), (6, 6), (45, 66), (37, 258)],
 }
+# lapgsrb's kernel (klap2.cuh) tiles 30 output rows per CTA: several row
+# tiles with ragged tails, and z extents the one-wave grid splits into parts
+LAP_SHAPES = {"f32": [(11, 67, 260), (40, 33, 516), (3, 95, 132)], "f64": [(9, 64, 130), (33, 31, 66)]}
 COEFFS = {"uxx1": [0.3, 1.2, -0.07], "lapgsrb": [0.15]}
 
 
@@ -38,7 +41,8 @@ def cases():
     for kind in ("tricubic2", "uxx1", "lapgsrb", "whispering"):
         need = 4 if kind in ("tricubic2", "uxx1") else 3
         for dt in ("f32", "f64"):
-            for shape in (SHAPES2 if kind == "whispering" else SHAPES3)[dt]:
+            extra = LAP_SHAPES[dt] if kind == "lapgsrb" else []
+            for shape in (SHAPES2 if kind == "whispering" else SHAPES3)[dt] + extra:
                 if min(shape) >= need:
                     yield kind, dt, shape
 
@@ -67,7 +71,7 @@ def test_step_parity_and_variants(oracle, kind, dtype, shape, coeffs):
 
 
 @pytest.mark.parametrize("kind,dtype,shape", [
-    ("lapgsrb", "f32", (21, 18, 260)), ("lapgsrb", "f64", (9, 10, 66)),
+    ("lapgsrb", "f32", (21, 18, 260)), ("lapgsrb", "f64", (9, 10, 66)), ("lapgsrb", "f32", (11, 67, 260)),
     ("uxx1", "f32", (19, 13, 132)), ("whispering", "f32", (70, 132)), ("tricubic2", "f32", (19, 13, 132))])
 def test_run_parity(oracle, kind, dtype, shape):
     """stencil_run: lapgsrb ping-pongs (Dirichlet ring held), the others
