@@ -76,20 +76,26 @@ struct Lap2Args {
 };
 
 // The arrival sequence of a CTA (one u plane each): pieces in LockIter
-// order, nseg + 4 planes per piece (u planes z_lo+zo-2 .. z_lo+zo+nseg+1).
+// order, nseg + 4 planes per piece (u planes z_lo+zo-2 .. z_lo+zo+nseg+1);
+// the box origin is computed once per piece.
 struct ProdIter {
     LockIter it;
-    int64_t col = 0;
-    int zo = 0, nseg = 0, t = 0;
-    bool live = false;
-    __device__ __forceinline__ bool next(int64_t& c, int& zrel) {   // zrel: plane - z_lo
-        if (!live || t >= nseg + 4) {
+    int ntx;
+    int bx = 0, by = 0, z = 0, left = 0;
+    __device__ __forceinline__ bool next(int TX, int TY, int padx, int z_lo, int& x, int& y, int& zz) {
+        if (left == 0) {
+            int64_t col;
+            int zo, nseg;
             if (!it.next(col, zo, nseg)) return false;
-            live = true;
-            t = 0;
+            bx = (int)(col % ntx) * TX - padx;
+            by = (int)(col / ntx) * TY - 2;
+            z = z_lo + zo - 2;
+            left = nseg + 4;
         }
-        c = col;
-        zrel = zo - 2 + t++;
+        x = bx;
+        y = by;
+        zz = z++;
+        --left;
         return true;
     }
 };
@@ -116,15 +122,13 @@ klapgsrb2(const __grid_constant__ TmapPack<1> tm, const __grid_constant__ Lap2Ar
     // iteration G has passed, stage G-3 is free and arrival G + NS - 3 is
     // issued into it.  (No producer warp: 16 warps keep 128 registers per
     // thread, a 17th would cap them at 96.)
-    ProdIter pit{LockIter(ncols, a.nzo, a.zsplit, a.zc, a.m, blockIdx.x, gridDim.x)};
+    ProdIter pit{LockIter(ncols, a.nzo, a.zsplit, a.zc, a.m, blockIdx.x, gridDim.x), a.ntx};
     auto produce = [&](uint32_t A) {
-        int64_t pc;
-        int pz;
-        if (!pit.next(pc, pz)) return;
+        int x, y, z;
+        if (!pit.next(TX, TY, PADX, a.z_lo, x, y, z)) return;
         const uint32_t s = A % NS;
         mbar_arrive_expect_tx(&full[s], (uint32_t)(L::BX * L::BY * sizeof(T)));
-        tma_load_3d(smem + (size_t)s * L::STAGE, &tm.m[0], (int)(pc % a.ntx) * TX - PADX,
-                    (int)(pc / a.ntx) * TY - 2, a.z_lo + pz, &full[s]);
+        tma_load_3d(smem + (size_t)s * L::STAGE, &tm.m[0], x, y, z, &full[s]);
     };
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
@@ -156,37 +160,68 @@ klapgsrb2(const __grid_constant__ TmapPack<1> tm, const __grid_constant__ Lap2Ar
     int zo, nseg;
     while (it.next(col, zo, nseg)) {
         const int tx = (int)(col % a.ntx), ty = (int)(col / a.ntx);
-        const int64_t x0 = (int64_t)tx * TX, xl = x0 + lane * V;
-        const int64_t y0 = (int64_t)ty * TY;
-        const bool own = xl < nx;
-        const bool x_vec = own && xl >= 1 && xl + V <= nx - 1;
+        const int nxi = (int)nx;                           // rows are < 2^31 elements
+        const int x0 = tx * TX, xl = x0 + lane * V;
+        const int y0 = ty * TY;
+        const bool own = xl < nxi;
+        const bool x_vec = own && xl >= 1 && xl + V <= nxi - 1;
+        // warp-uniform: every element of the tile row is interior in x (all
+        // but the grid-edge tiles), so the red updates need no x mask
+        const bool xall = __all_sync(FULL, x_vec);
         bool xin[V];
 #pragma unroll
-        for (int e = 0; e < V; ++e) xin[e] = xl + e >= 1 && xl + e <= nx - 2;
-        // the lane's corner point (lane 0: x0-1, the others: x0+TX; lane 31's is used)
-        const int64_t xe = lane0 ? x0 - 1 : x0 + TX;
-        const bool xe_in = xe >= 1 && xe <= nx - 2;
-        const int ce = PADX + (lane0 ? -1 : TX);           // its column in the u box
-        int64_t gy[RY];
-        bool yin[RY], out_ok[RY];
+        for (int e = 0; e < V; ++e) xin[e] = xl + e >= 1 && xl + e <= nxi - 2;
+        // corner point k = lane & 3 of this warp: row rho_k = 2*warp + (k & 1),
+        // left (x0-1, k < 2) or right (x0+TX) of the tile; lanes 4..31 repeat
+        // lanes 0..3 (same value, same address)
+        const int ck = lane & 3, krr = ck & 1, kside = ck >> 1;
+        const int xe = kside ? x0 + TX : x0 - 1;
+        const bool xe_in = xe >= 1 && xe <= nxi - 2;
+        const int xe_odd = kside ? 0 : 1;                  // x0 is even
+        const int ce = (warp * RY + krr + 1) * BX + PADX + (kside ? TX : -1);   // in the u box
+        const int cre = (warp * RY + krr) * RX + (kside ? RPAD + TX : RPAD - 1); // in the r plane
+        // warp-edge fallback column of the SHUFFLE variant (lane 0: x0-1, lane 31: x0+TX)
+        const int fb = PADX + (lane0 ? -1 : TX);
+        const int frb = lane0 ? RPAD - 1 : RPAD + TX;
+        int gy[RY];
+        bool yin[RY], out_ok[RY], act[RY][V];
 #pragma unroll
         for (int rr = 0; rr < RY; ++rr) {
             const int rho = warp * RY + rr;
             gy[rr] = y0 - 1 + rho;
-            yin[rr] = gy[rr] >= 1 && gy[rr] <= ny - 2;
+            yin[rr] = gy[rr] >= 1 && gy[rr] <= (int)ny - 2;
             out_ok[rr] = yin[rr] && rho >= 1 && rho <= TY;
-        }
-        const int64_t Z0 = (int64_t)a.z_lo + zo - 2;        // u plane of arrival 0
-        const int np = nseg + 4;
-
-        // unrolled by 3 so that the queue slots (arrival % 3) are compile-time
-        for (int tb = 0; tb < np; tb += 3) {
 #pragma unroll
-        for (int u = 0; u < 3; ++u) {
-            const int t = tb + u;
-            if (t >= np) break;
+            for (int e = 0; e < V; ++e) act[rr][e] = yin[rr] && (xall || xin[e]);
+        }
+        const int yk = y0 - 1 + warp * RY + krr;
+        const bool ck_in = xe_in && yk >= 1 && yk <= (int)ny - 2;   // corner point inside the grid interior (x, y)
+        // warp-uniform: both rows interior in y and every element in x (the
+        // red updates then need no mask)
+        const bool fast = xall && yin[0] && yin[1];
+        bool st_fast[RY];
+#pragma unroll
+        for (int rr = 0; rr < RY; ++rr) st_fast[rr] = xall && out_ok[rr];
+        const int Z0 = a.z_lo + zo - 2;                     // u plane of arrival 0
+        const int np = nseg + 4;
+        T* obase[RY];
+#pragma unroll
+        for (int rr = 0; rr < RY; ++rr) obase[rr] = a.out + ((int64_t)(Z0 + 2) * ny + gy[rr]) * nx + xl;
+        // the two rows of a warp have opposite colours: par0 = colour of row 0
+        const int par0 = (gy[0] + Z0) & 1;                  // at u plane Z0
+
+        // One arrival t (u plane Z0 + t): the centre rows into the queue;
+        // S1: r at plane zr = Z0 + t - 1 (u planes t-2, t-1, t); S2: output
+        // plane zr - 1 (r planes t-2, t-1, t).  U = t % 3 (queue slots).
+        // Both stages' operands are gathered first and their arithmetic
+        // shares one colour branch (plane zr and zr - 1 have opposite
+        // colours), so the two stages interleave.
+        auto arrival = [&](int t, auto U, auto S1, auto S2) {
+            constexpr int u = decltype(U)::value;
+            constexpr bool s1on = decltype(S1)::value, s2on = decltype(S2)::value;
+            constexpr int s0 = u, s1 = (u + 2) % 3, s2 = (u + 1) % 3;   // slots of t, t-1, t-2
             mbar_wait(&full[G % NS], (G / NS) & 1u);
-            // every warp has finished iteration t-1: the r plane written two
+            // every warp has finished arrival t-1: the r plane written two
             // planes ago is free again, and u stage G-3 is read by no one
             lap_bar();
             if (threadIdx.x == 0) {
@@ -195,139 +230,186 @@ klapgsrb2(const __grid_constant__ TmapPack<1> tm, const __grid_constant__ Lap2Ar
             }
             const T* sp = stage(G);
             const uint32_t Gc = G++;
-            const int s0 = u, s1 = (u + 2) % 3, s2 = (u + 1) % 3;   // slots of t, t-1, t-2 (unrolled: constants)
 #pragma unroll
             for (int rr = 0; rr < RY; ++rr)
                 lds_vec(sp + (warp * RY + rr + 1) * BX + PADX + lane * V, uq[rr][s0]);
-            if (t < 2) continue;
-
-            // ---- stage 1: r at plane zr = Z0 + t - 1 (u planes t-2, t-1, t)
-            const int64_t zr = Z0 + t - 1;
-            const bool zin = zr >= 1 && zr <= nz - 2;
-            const T* sc = stage(Gc - 1);
-            const T* sm = stage(Gc - 2);
-            T* rp = rplane(zr);
-#pragma unroll
-            for (int rr = 0; rr < RY; ++rr) {
-                const int rho = warp * RY + rr, row = rho + 1;     // box row of the r row
-                const T* c = uq[rr][s1];
-                T ym[V], yp[V];
-                if (rr == 0) lds_vec(sc + (row - 1) * BX + PADX + lane * V, ym);
-                else {
-#pragma unroll
-                    for (int e = 0; e < V; ++e) ym[e] = uq[0][s1][e];
+            if constexpr (s1on) {
+                const int zr = Z0 + t - 1;
+                const bool zin = zr >= 1 && zr <= (int)nz - 2;
+                const T* sc = stage(Gc - 1);
+                const T* sm = stage(Gc - 2);
+                T* rp = rplane(zr);
+                {   // the warp's four corner points (both variants: S2 reads them from the r plane)
+                    T s = sc[ce - 1] + sc[ce + 1];
+                    s = s + sc[ce - BX];
+                    s = s + sc[ce + BX];
+                    s = s + sm[ce];
+                    s = s + sp[ce];
+                    const bool red = ((xe_odd + yk + zr) & 1) == 0;
+                    rp[cre] = red && ck_in && zin ? w * s : sc[ce];
                 }
-                if (rr == RY - 1) lds_vec(sc + (row + 1) * BX + PADX + lane * V, yp);
-                else {
+                // S1 operands: y taps, x halo of u
+                T ym[RY][V], yp[RY][V], xm[RY], xp[RY];
 #pragma unroll
-                    for (int e = 0; e < V; ++e) yp[e] = uq[1][s1][e];
-                }
-                T xm, xp;
-                if constexpr (VARIANT == 0) {
-                    xm = shfl_up(c[V - 1], 1);
-                    xp = shfl_down(c[0], 1);
-                } else {
-                    xm = sc[row * BX + PADX + lane * V - 1];
-                    xp = sc[row * BX + PADX + lane * V + V];
-                }
-                // corner point of the lane (both variants: stage 2 reads it from the r plane)
-                T cl, cc, cr;
-                {
-                    const T* pr = sc + row * BX + PADX + (lane0 ? -2 : TX);
-                    T p0, p1;
-                    if constexpr (sizeof(T) == 4) {
-                        const float2 t2 = *reinterpret_cast<const float2*>(pr);
-                        p0 = t2.x; p1 = t2.y;
+                for (int rr = 0; rr < RY; ++rr) {
+                    const int row = warp * RY + rr + 1;   // box row of the r row
+                    const T* c = uq[rr][s1];
+                    if (rr == 0) lds_vec(sc + (row - 1) * BX + PADX + lane * V, ym[rr]);
+                    else {
+#pragma unroll
+                        for (int e = 0; e < V; ++e) ym[rr][e] = uq[0][s1][e];
+                    }
+                    if (rr == RY - 1) lds_vec(sc + (row + 1) * BX + PADX + lane * V, yp[rr]);
+                    else {
+#pragma unroll
+                        for (int e = 0; e < V; ++e) yp[rr][e] = uq[1][s1][e];
+                    }
+                    if constexpr (VARIANT == 0) {
+                        xm[rr] = shfl_up(c[V - 1], 1);
+                        xp[rr] = shfl_down(c[0], 1);
+                        const T f = sc[row * BX + fb];        // the warp-edge fallback load
+                        xm[rr] = lane0 ? f : xm[rr];
+                        xp[rr] = lane == 31 ? f : xp[rr];
                     } else {
-                        p0 = pr[0]; p1 = pr[1];
-                    }
-                    cl = lane0 ? p0 : c[V - 1];
-                    cc = lane0 ? p1 : p0;
-                    cr = lane0 ? c[0] : p1;
-                    if constexpr (VARIANT == 0) {                  // the warp-edge fallback loads
-                        if (lane0) xm = p1;
-                        if (lane == 31) xp = p0;
+                        xm[rr] = sc[row * BX + PADX + lane * V - 1];
+                        xp[rr] = sc[row * BX + PADX + lane * V + V];
                     }
                 }
-                {
-                    T s = cl + cr;
-                    s = s + sc[(row - 1) * BX + ce];
-                    s = s + sc[(row + 1) * BX + ce];
-                    s = s + sm[row * BX + ce];
-                    s = s + sp[row * BX + ce];
-                    const bool red = ((xe + gy[rr] + zr) & 1) == 0;
-                    const T re = red && xe_in && yin[rr] && zin ? w * s : cc;
-                    if (lane0) rp[rho * RX + RPAD - 1] = re;
-                    if (lane == 31) rp[rho * RX + RPAD + TX] = re;
-                }
-                T r[V];
+                // S2 operands: y taps and x halo of r at plane zr - 1
+                const T* rc = rplane(zr - 1);              // complete: written before this arrival's barrier
+                T qm[RY][V], qp[RY][V], wm[RY], wp[RY];
+                if constexpr (s2on) {
 #pragma unroll
-                for (int e = 0; e < V; ++e) {
-                    T s = (e > 0 ? c[e - 1] : xm) + (e + 1 < V ? c[e + 1] : xp);
-                    s = s + ym[e];
-                    s = s + yp[e];
-                    s = s + uq[rr][s2][e];
-                    s = s + uq[rr][s0][e];
-                    const bool red = ((e + gy[rr] + zr) & 1) == 0;     // xl is even
-                    r[e] = red && xin[e] && yin[rr] && zin ? w * s : c[e];
-                    rq[rr][s0][e] = r[e];
+                    for (int rr = 0; rr < RY; ++rr) {
+                        const int rho = warp * RY + rr;
+                        const T* c = rq[rr][s1];
+                        if (rr == 0) lds_vec(rc + (rho > 0 ? rho - 1 : 0) * RX + RPAD + lane * V, qm[rr]);
+                        else {
+#pragma unroll
+                            for (int e = 0; e < V; ++e) qm[rr][e] = rq[0][s1][e];
+                        }
+                        if (rr == RY - 1) lds_vec(rc + (rho + 1 < NR ? rho + 1 : rho) * RX + RPAD + lane * V, qp[rr]);
+                        else {
+#pragma unroll
+                            for (int e = 0; e < V; ++e) qp[rr][e] = rq[1][s1][e];
+                        }
+                        if constexpr (VARIANT == 0) {
+                            wm[rr] = shfl_up(c[V - 1], 1);
+                            wp[rr] = shfl_down(c[0], 1);
+                            const T f = rc[rho * RX + frb];   // corner r (the fallback load)
+                            wm[rr] = lane0 ? f : wm[rr];
+                            wp[rr] = lane == 31 ? f : wp[rr];
+                        } else {
+                            wm[rr] = rc[rho * RX + RPAD + lane * V - 1];
+                            wp[rr] = rc[rho * RX + RPAD + lane * V + V];
+                        }
+                    }
                 }
-                st_vec_s(rp + rho * RX + RPAD + lane * V, r);
+                // element e of row rr is red at plane zr iff (e + rr + P) is
+                // even, P = colour of row 0 at zr (xl is even; warp-uniform).
+                // S1: r = w*nb6(u) at red elements, u elsewhere.  S2 (plane
+                // zr - 1, opposite colours): the black outputs are w times
+                // the sum of their six new red neighbours, the red ones r.
+                T r[RY][V], o[RY][V];
+#pragma unroll
+                for (int rr = 0; rr < RY; ++rr)
+#pragma unroll
+                    for (int e = 0; e < V; ++e) {
+                        r[rr][e] = uq[rr][s1][e];
+                        o[rr][e] = rq[rr][s1][e];
+                    }
+                auto upd = [&](auto P) {
+                    constexpr int pz = decltype(P)::value;
+#pragma unroll
+                    for (int rr = 0; rr < RY; ++rr) {
+                        const T* c = uq[rr][s1];
+#pragma unroll
+                        for (int e = 0; e < V; ++e) {
+                            if (((e + rr + pz) & 1) != 0) continue;
+                            T s = (e > 0 ? c[e - 1] : xm[rr]) + (e + 1 < V ? c[e + 1] : xp[rr]);
+                            s = s + ym[rr][e];
+                            s = s + yp[rr][e];
+                            s = s + uq[rr][s2][e];
+                            s = s + uq[rr][s0][e];
+                            r[rr][e] = w * s;
+                        }
+                    }
+                    T ps[RY][V];                           // S2: the first five taps
+                    if constexpr (s2on) {
+#pragma unroll
+                        for (int rr = 0; rr < RY; ++rr) {
+                            const T* c = rq[rr][s1];
+#pragma unroll
+                            for (int e = 0; e < V; ++e) {
+                                if (((e + rr + pz) & 1) != 0) continue;   // black at zr - 1
+                                T s = (e > 0 ? c[e - 1] : wm[rr]) + (e + 1 < V ? c[e + 1] : wp[rr]);
+                                s = s + qm[rr][e];
+                                s = s + qp[rr][e];
+                                ps[rr][e] = s + rq[rr][s2][e];
+                            }
+                        }
+                    }
+                    // outside the interior r = u (rare: grid-edge tiles and planes)
+                    if (!(fast && zin)) {
+#pragma unroll
+                        for (int rr = 0; rr < RY; ++rr)
+#pragma unroll
+                            for (int e = 0; e < V; ++e) r[rr][e] = zin && act[rr][e] ? r[rr][e] : uq[rr][s1][e];
+                    }
+                    if constexpr (s2on) {
+#pragma unroll
+                        for (int rr = 0; rr < RY; ++rr)
+#pragma unroll
+                            for (int e = 0; e < V; ++e) {
+                                if (((e + rr + pz) & 1) != 0) continue;
+                                o[rr][e] = w * (ps[rr][e] + r[rr][e]);   // + r at plane zr (red there)
+                            }
+                    }
+                };
+                if (((par0 + t - 1) & 1) == 0) upd(std::integral_constant<int, 0>{});
+                else upd(std::integral_constant<int, 1>{});
+#pragma unroll
+                for (int rr = 0; rr < RY; ++rr) {
+#pragma unroll
+                    for (int e = 0; e < V; ++e) rq[rr][s0][e] = r[rr][e];
+                    st_vec_s(rp + (warp * RY + rr) * RX + RPAD + lane * V, r[rr]);
+                }
+                if constexpr (s2on) {
+#pragma unroll
+                    for (int rr = 0; rr < RY; ++rr) {
+                        T* op = obase[rr];
+                        obase[rr] += plane;
+                        if (st_fast[rr]) stg_vec(op, o[rr]);
+                        else if (out_ok[rr]) {
+                            if (x_vec) stg_vec(op, o[rr]);
+                            else if (own) {
+#pragma unroll
+                                for (int e = 0; e < V; ++e)
+                                    if (xin[e]) op[e] = o[rr][e];
+                            }
+                        }
+                    }
+                }
             }
-            if (t < 4) continue;
-
-            // ---- stage 2: output plane zo_ = zr - 1 (r planes t-2, t-1, t)
-            const int64_t zo_ = zr - 1;
-            const T* rc = rplane(zo_);                     // complete: written before this plane's barrier
-#pragma unroll
-            for (int rr = 0; rr < RY; ++rr) {
-                const int rho = warp * RY + rr;
-                const T* c = rq[rr][s1];
-                T ym[V], yp[V];
-                if (rr == 0) lds_vec(rc + (rho > 0 ? rho - 1 : 0) * RX + RPAD + lane * V, ym);
-                else {
-#pragma unroll
-                    for (int e = 0; e < V; ++e) ym[e] = rq[0][s1][e];
-                }
-                if (rr == RY - 1) lds_vec(rc + (rho + 1 < NR ? rho + 1 : rho) * RX + RPAD + lane * V, yp);
-                else {
-#pragma unroll
-                    for (int e = 0; e < V; ++e) yp[e] = rq[1][s1][e];
-                }
-                T xm, xp;
-                if constexpr (VARIANT == 0) {
-                    xm = shfl_up(c[V - 1], 1);
-                    xp = shfl_down(c[0], 1);
-                    const T pe = rc[rho * RX + (lane0 ? RPAD - 1 : RPAD + TX)];
-                    if (lane0) xm = pe;
-                    if (lane == 31) xp = pe;
-                } else {
-                    xm = rc[rho * RX + RPAD + lane * V - 1];
-                    xp = rc[rho * RX + RPAD + lane * V + V];
-                }
-                T o[V];
-#pragma unroll
-                for (int e = 0; e < V; ++e) {
-                    T s = (e > 0 ? c[e - 1] : xm) + (e + 1 < V ? c[e + 1] : xp);
-                    s = s + ym[e];
-                    s = s + yp[e];
-                    s = s + rq[rr][s2][e];
-                    s = s + rq[rr][s0][e];
-                    const bool red = ((e + gy[rr] + zo_) & 1) == 0;
-                    o[e] = red ? c[e] : w * s;
-                }
-                if (out_ok[rr]) {
-                    T* op = a.out + (zo_ * ny + gy[rr]) * nx + xl;
-                    if (x_vec) stg_vec(op, o);
-                    else if (own) {
-#pragma unroll
-                        for (int e = 0; e < V; ++e)
-                            if (xin[e]) op[e] = o[e];
-                    }
-                }
-            }
+        };
+        using BT = std::true_type;
+        using BF = std::false_type;
+        using I0 = std::integral_constant<int, 0>;
+        using I1 = std::integral_constant<int, 1>;
+        using I2 = std::integral_constant<int, 2>;
+        // prologue (np >= 5): queue only, then r only
+        arrival(0, I0{}, BF{}, BF{});
+        arrival(1, I1{}, BF{}, BF{});
+        arrival(2, I2{}, BT{}, BF{});
+        arrival(3, I0{}, BT{}, BF{});
+        int t = 4;                                         // slots: t % 3 == 1, 2, 0
+        for (; t + 3 <= np; t += 3) {
+            arrival(t, I1{}, BT{}, BT{});
+            arrival(t + 1, I2{}, BT{}, BT{});
+            arrival(t + 2, I0{}, BT{}, BT{});
         }
-        }
+        if (t < np) arrival(t, I1{}, BT{}, BT{});
+        if (t + 1 < np) arrival(t + 1, I2{}, BT{}, BT{});
     }
     (void)plane;
 }
