@@ -214,8 +214,6 @@ static cudaError_t launch_lap2(const stencil_s* h, const void* const* in, void* 
     if (z_lo < 0) { z_lo = 1; z_hi = ld[2] - 1; }
     if (z_hi <= z_lo) return cudaSuccess;
     TmapPack<1> tm;
-    cudaError_t e = make_tmap(&tm.m[0], in[0], h->dtype, ld, L::BX, L::BY);
-    if (e != cudaSuccess) return e;
     Lap2Args<T> args{};
     args.out = (T*)out[0];
     args.nx = ld[0];
@@ -224,20 +222,45 @@ static cudaError_t launch_lap2(const stencil_s* h, const void* const* in, void* 
     args.z_lo = (int)z_lo;
     args.nzo = (int)(z_hi - z_lo);
     args.ntx = (int)((ld[0] + L::TX - 1) / L::TX);
-    args.nty = (int)((ld[1] + L::TY - 1) / L::TY);
-    const int64_t ncols = (int64_t)args.ntx * args.nty;
     const int64_t slots = (int64_t)bps * sm_count_of(h->device);
-    int64_t zsplit = slots / ncols;
-    if (zsplit < 1) zsplit = 1;
-    if (zsplit > args.nzo) zsplit = args.nzo;
-    const int64_t items = ncols * zsplit;
-    const int64_t m = (items + slots - 1) / slots;
-    const int64_t grid = (items + m - 1) / m;
-    args.zsplit = (int)zsplit;
-    args.m = (int)m;
+    // tile height: the even ty <= TY that maximises (useful rows of the
+    // tiles) x (staged rows that are outputs, ty / (ty + 4)) x (busy SMs of
+    // the one-wave grid); e.g. 1024 rows x 4 x-tiles -> ty = 28: 37 x 4 =
+    // 148 columns on 148 SMs instead of 35 x 4 = 140 at ty = 30
+    static const int ty_env = getenv("STB200_LAP_TY") ? atoi(getenv("STB200_LAP_TY")) : 0;
+    double best = -1.0;
+    int64_t best_zsplit = 1, best_m = 1;
+    for (int ty = L::TY; ty >= 8; ty -= 2) {
+        if (ty_env > 0 && ty != ty_env) continue;
+        const int64_t nty = (ld[1] + ty - 1) / ty;
+        const int64_t ncols = (int64_t)args.ntx * nty;
+        int64_t zsplit = slots / ncols;
+        if (zsplit < 1) zsplit = 1;
+        if (zsplit > args.nzo) zsplit = args.nzo;
+        const int64_t items = ncols * zsplit;
+        const int64_t m = (items + slots - 1) / slots;
+        const double rows_eff = (double)(ld[1] - 2) / (double)(nty * ty);
+        const double stage_eff = (double)ty / (ty + 4);
+        const double util = (double)items / (double)(m * slots);
+        const double score = rows_eff * stage_eff * util;
+        if (score > best + 1e-9) {
+            best = score;
+            args.ty = ty;
+            args.nty = (int)nty;
+            best_zsplit = zsplit;
+            best_m = m;
+        }
+    }
+    if (best < 0) return cudaErrorInvalidValue;
+    const int64_t items = (int64_t)args.ntx * args.nty * best_zsplit;
+    const int64_t grid = (items + best_m - 1) / best_m;
+    args.zsplit = (int)best_zsplit;
+    args.m = (int)best_m;
     static const int zc_env = getenv("STB200_LAP_ZC") ? atoi(getenv("STB200_LAP_ZC")) : 0;
     args.zc = zc_env > 0 ? zc_env : 64;
     args.w = (T)h->coeffs[0];
+    cudaError_t e = make_tmap(&tm.m[0], in[0], h->dtype, ld, L::BX, args.ty + 4);
+    if (e != cudaSuccess) return e;
     kern<<<(unsigned)grid, klap2_threads(), L::SMEM, s>>>(tm, args);
     return cudaGetLastError();
 }

@@ -46,7 +46,7 @@ template <typename T>
 struct LapLayout {
     static constexpr int V = vlen<T>(), TX = 32 * V;
     static constexpr int RY = 2, NR = kLapWarps * RY;      // r rows per tile
-    static constexpr int TY = NR - 2;                      // output rows per tile
+    static constexpr int TY = NR - 2;                      // output rows per tile (at most; Lap2Args::ty)
     static constexpr int PADX = 32 / (int)sizeof(T);       // u box x pad (one sector)
     static constexpr int BX = TX + 2 * PADX, BY = NR + 2;  // u box: rows y0-2 .. y0+NR-1
     static constexpr int STAGE = (BX * BY * (int)sizeof(T) + 127) / 128 * 128;
@@ -71,6 +71,7 @@ struct Lap2Args {
     int64_t nx, ny, nz;
     int z_lo, nzo;          // output planes [z_lo, z_lo + nzo)
     int ntx, nty;
+    int ty;                 // output rows per tile (even, <= LapLayout::TY): the u box has ty + 4 rows
     int zsplit, zc, m;      // LockIter
     T w;
 };
@@ -108,7 +109,9 @@ template <typename T, int VARIANT>
 __global__ void __launch_bounds__(klap2_threads(), 1)
 klapgsrb2(const __grid_constant__ TmapPack<1> tm, const __grid_constant__ Lap2Args<T> a) {
     using L = LapLayout<T>;
-    constexpr int V = L::V, TX = L::TX, NS = L::NS, RY = L::RY, TY = L::TY, NR = L::NR;
+    constexpr int V = L::V, TX = L::TX, NS = L::NS, RY = L::RY, NR = L::NR;
+    const int TY = a.ty;                                   // runtime tile height (dispatch3d.cu picks it)
+    const uint32_t box_bytes = (uint32_t)(L::BX * (TY + 4) * sizeof(T));
     constexpr int BX = L::BX, PADX = L::PADX, RX = L::RX, RPAD = L::RPAD;
 
     extern __shared__ __align__(128) unsigned char smem[];
@@ -127,7 +130,7 @@ klapgsrb2(const __grid_constant__ TmapPack<1> tm, const __grid_constant__ Lap2Ar
         int x, y, z;
         if (!pit.next(TX, TY, PADX, a.z_lo, x, y, z)) return;
         const uint32_t s = A % NS;
-        mbar_arrive_expect_tx(&full[s], (uint32_t)(L::BX * L::BY * sizeof(T)));
+        mbar_arrive_expect_tx(&full[s], box_bytes);
         tma_load_3d(smem + (size_t)s * L::STAGE, &tm.m[0], x, y, z, &full[s]);
     };
     if (threadIdx.x == 0) {
@@ -230,6 +233,8 @@ klapgsrb2(const __grid_constant__ TmapPack<1> tm, const __grid_constant__ Lap2Ar
             }
             const T* sp = stage(G);
             const uint32_t Gc = G++;
+            // (warps whose rows lie beyond a shorter tile compute unused rows:
+            // skipping them with an early exit measured 12% slower overall)
 #pragma unroll
             for (int rr = 0; rr < RY; ++rr)
                 lds_vec(sp + (warp * RY + rr + 1) * BX + PADX + lane * V, uq[rr][s0]);
