@@ -50,6 +50,9 @@ typedef struct stencil_s* stencil_t;
  *  ST_JACOBI2D9     in -> out, r=1   Listing 5       coeffs (c0,c1,c2)    default (1/4,1/8,1/16)
  *  ST_GAUSSBLUR5X5  in -> out, r=2   Table 1 gaussblur, 25 loads        25 weights w[dj][di] default binomial/256
  *  ST_GAMEOFLIFE    in -> out, r=1   Table 1 gameoflife, int32 B3/S23   none
+ *                   (cells are Life states 0 / 1; the streaming multi-sweep
+ *                   kernel packs four cells per register and reads a cell as
+ *                   its lowest bit, so only 0/1 grids are defined)
  *  ST_LAPLACIAN3D7  in -> out, r=1   Table 1 laplacian, 7 loads         coeffs (a,b)         default (-6, 1)
  *  ST_JACOBI3D7     in -> out, r=1   laplacian form, Jacobi weights     coeffs (a,b)         default (0, 1/6)
  *  ST_WAVE13PT      (prev,cur) -> next, r=2  Table 1 wave13pt, 14 loads coeffs (m0,m1,m2)    default lambda=1/8
@@ -134,8 +137,8 @@ int stencil_get_variant(stencil_t h, int* variant);
  * single sweeps.
  *   0 (default) auto: grids that sit in L2 (<= 8 MiB per buffer) run the
  *                     on-chip kernels (per-launch latency bounds those runs);
- *                     larger jacobi2d5 grids run the streaming three-sweep
- *                     register-cache kernel, jacobi2d9 / gameoflife the
+ *                     larger jacobi2d5 / gameoflife grids run the streaming
+ *                     three-sweep register-cache kernel, jacobi2d9 the
  *                     two-sweep one (one HBM pass per two or three sweeps:
  *                     the single-sweep kernel is HBM-bound); gaussblur keeps
  *                     one sweep per launch (issue-bound at two sweeps per

@@ -380,9 +380,12 @@ static int pair_fusion(const stencil_s* h, int n_iters) {
     const int k = h->k->kind;
     const bool cheap = k == ST_JACOBI2D5 || k == ST_JACOBI2D9 || k == ST_GAMEOFLIFE;
     // three sweeps per launch for jacobi2d5 (measured: 32768^2 fp32 1595 ->
-    // 1792 Gpt/s SHUFFLE, fp64 +8%); jacobi2d9 and gameoflife run slower at
-    // three (issue), gaussblur has no three-sweep kernel
-    int nsw = k == ST_JACOBI2D5 ? 3 : 2;
+    // 1792 Gpt/s SHUFFLE, fp64 +8%); jacobi2d9 runs slower at three (issue),
+    // gaussblur has no three-sweep kernel
+    // gameoflife: three with the packed kernel (klife.cuh: 16384^2 1490 -> 1799
+    // Gpt/s SHUFFLE, 1505 -> 1862 PLAIN; the int32 form is issue-bound at two)
+    static const int life_int = getenv("STB200_LIFE_INT") ? atoi(getenv("STB200_LIFE_INT")) : 0;
+    int nsw = k == ST_JACOBI2D5 || (k == ST_GAMEOFLIFE && !life_int) ? 3 : 2;
     if (cheap && env_nsw >= 2 && env_nsw <= 3) nsw = env_nsw;
     if (h->fusion == 2 || h->fusion == 3) nsw = h->fusion;   // forced: exactly that many
     if (nsw > n_iters) nsw = n_iters;
@@ -491,8 +494,12 @@ extern "C" int stencil_run(stencil_t h, void* const* bufs, int n_iters, void* st
     int result = 0;
 
     // Multi-GPU runs are enqueued directly: the NCCL calls inside each step
-    // are issued on a side stream with events (see dist.cu).
-    if (h->dist) {
+    // are issued on a side stream with events (see dist.cu).  So is a run
+    // that is ONE kernel launch (all sweeps of a small 2-D run in ktb2r,
+    // no ring copy): a graph would only add its launch latency.
+    const bool one_launch = h->k->iterable == 1 && n_iters >= 1 && !pair_fusion(h, n_iters) &&
+                            fusion_depth(h, n_iters) >= n_iters;
+    if (h->dist || one_launch) {
         int rc = enqueue_run(h, bufs, n_iters, s, &result);
         if (!rc && result_idx) *result_idx = result;
         return rc;

@@ -7,6 +7,7 @@
 #include "ktb2d.cuh"
 #include "ktb2r.cuh"
 #include "k2d2.cuh"
+#include "klife.cuh"
 
 namespace stb200 {
 
@@ -213,8 +214,41 @@ static cudaError_t launch_fused(const stencil_s* h, const void* in, void* out, c
     return launch_tb<Op, T>(h, in, out, s, S);
 }
 
+// gameoflife, packed four cells per register (klife.cuh); launch geometry as launch_k2d2
+template <int VAR, int NSW>
+static cudaError_t launch_life(const stencil_s* h, const void* in, void* out, cudaStream_t s) {
+    constexpr int kStripH = 128;
+    auto kern = k2dlife<VAR, NSW>;
+    constexpr size_t smem = k2d2_smem_bytes<int, NSW>();
+    kernel_setup((const void*)kern, h->device, smem, k2d_threads());
+    const int64_t nx = h->ldims[0], ny = h->ldims[1];
+    const int64_t y_lo = 1, y_hi = ny - 1;
+    if (y_hi <= y_lo) return cudaSuccess;
+    const int64_t gx = (nx + kWarps2D * k2d2_txo<int, NSW>() - 1) / (kWarps2D * k2d2_txo<int, NSW>());
+    const int64_t rows = y_hi - y_lo;
+    static const int dbg_h = getenv("STB200_2D2_H") ? atoi(getenv("STB200_2D2_H")) : 0;
+    int64_t H = (rows * gx + 2 * sm_count(h->device) - 1) / (2 * sm_count(h->device));
+    H = H < 4 ? 4 : H > kStripH ? kStripH : H;
+    if (dbg_h > 0) H = dbg_h;
+    const int64_t nstrips = (rows + H - 1) / H;
+    if (nstrips > 65535 || ny > INT32_MAX) return cudaErrorInvalidConfiguration;
+    kern<<<dim3((unsigned)gx, (unsigned)nstrips), k2d_threads(), smem, s>>>(
+        (const int*)in, (int*)out, nx, (int)ny, (int)y_lo, (int)y_hi, (int)H);
+    return cudaGetLastError();
+}
+
 template <class Op, typename T>
 static cudaError_t pair_op(const stencil_s* h, const void* in, void* out, cudaStream_t s, int nsw) {
+    // gameoflife: the packed kernel (klife.cuh); STB200_LIFE_INT=1 selects
+    // the int32 k2d2 form for A/B runs
+    static const int life_int = getenv("STB200_LIFE_INT") ? atoi(getenv("STB200_LIFE_INT")) : 0;
+    if constexpr (std::is_same<Op, OpLife>::value) {
+        if (!life_int) {
+            if (h->variant == ST_PLAIN)
+                return nsw == 3 ? launch_life<VAR_PLAIN, 3>(h, in, out, s) : launch_life<VAR_PLAIN, 2>(h, in, out, s);
+            return nsw == 3 ? launch_life<VAR_SHUFFLE, 3>(h, in, out, s) : launch_life<VAR_SHUFFLE, 2>(h, in, out, s);
+        }
+    }
     if (h->variant == ST_PLAIN)
         return nsw == 3 ? launch_k2d2<Op, T, VAR_PLAIN, 3>(h, in, out, s) : launch_k2d2<Op, T, VAR_PLAIN, 2>(h, in, out, s);
     return nsw == 3 ? launch_k2d2<Op, T, VAR_SHUFFLE, 3>(h, in, out, s) : launch_k2d2<Op, T, VAR_SHUFFLE, 2>(h, in, out, s);

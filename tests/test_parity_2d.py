@@ -76,10 +76,11 @@ def test_run_parity(oracle, kind, dtype, shape):
 @pytest.mark.parametrize("kind,dtype,shape", [
     ("jacobi2d5", "f32", (61, 132)), ("jacobi2d9", "f64", (45, 130)),
     ("gaussblur5x5", "f32", (77, 1028)), ("gaussblur5x5", "f64", (33, 258)),
-    ("gameoflife", "i32", (130, 260)), ("jacobi2d5", "f32", (3, 4))])
+    ("gameoflife", "i32", (130, 260)), ("gameoflife", "i32", (67, 1156)), ("jacobi2d5", "f32", (3, 4))])
 @pytest.mark.parametrize("fusion,n", [(0, 7), (2, 7), (2, 10), (2, 1), (3, 10), (3, 8), (-3, 10),
                                       (-16, 11), (-4, 1)])
-def test_fused_runs_bit_identical(oracle, kind, dtype, shape, fusion, n):
+@pytest.mark.parametrize("variant", ["shuffle", "plain"])
+def test_fused_runs_bit_identical(oracle, kind, dtype, shape, fusion, n, variant):
     """Temporal blocking (stencil_set_fusion: 2 / 3 = streaming kernel with
     two / three sweeps per launch, -S = shared-memory tile kernel, 0 =
     auto): the reported result buffer holds the same bits as single sweeps,
@@ -93,7 +94,7 @@ def test_fused_runs_bit_identical(oracle, kind, dtype, shape, fusion, n):
     ridx = oracle.run(kind, dtype, bufs, n)
     res = {}
     for fu in (1, fusion):
-        st = Stencil(kind, shape[::-1], dtype)
+        st = Stencil(kind, shape[::-1], dtype, variant=variant)
         st.set_fusion(fu)
         d = [torch.from_numpy(f.copy()).cuda(), torch.zeros(shape, dtype=torch.from_numpy(f).dtype,
                                                            device="cuda")]
@@ -103,7 +104,7 @@ def test_fused_runs_bit_identical(oracle, kind, dtype, shape, fusion, n):
             assert idx == ridx
         res[fu] = d[idx].cpu().numpy()
         st.close()
-    assert_parity(res[fusion], bufs[ridx], dtype, f"{kind} fused {fusion}")
+    assert_parity(res[fusion], bufs[ridx], dtype, f"{kind} fused {fusion} {variant}")
     assert np.array_equal(res[fusion].view(np.uint8), res[1].view(np.uint8))
 
 
