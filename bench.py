@@ -352,6 +352,8 @@ def main():
                     help="run one rank's share of an N-way strong-scaled slab on this GPU (attached "
                          "group of one with the slowest axis divided by N): the per-rank latency floor")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fusion", type=int, default=None,
+                    help="stencil_set_fusion value (A/B runs; default: the library's auto choice)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -406,6 +408,8 @@ def main():
             dist, torch, dist_get_id)
     else:
         st = Stencil(wl["kind"], dims, wl["dtype"], variant=args.variant)
+    if args.fusion is not None:
+        st.set_fusion(args.fusion)
     info = st.info()
     n_in, n_out, n_bufs = st.arity()
     ldims = info["local_dims"][: len(dims)]
@@ -484,7 +488,9 @@ def main():
     alg_bytes = info["bytes_per_point"] * pts_rank              # per launch on this rank
     achieved = alg_bytes / avg_launch_s / 1e9
     peak, peak_src = measured_peaks()
-    traffic = profile_traffic(args.workload, args.variant)
+    # dram bytes of the dominant kernel's launch: the multi-sweep kernel's
+    # capture (<workload>_pair) when the run fuses sweeps
+    traffic = profile_traffic(args.workload + ("_pair" if spl > 1 else ""), args.variant)
 
     # kernel-only timing: individual stencil_step launches bracketed by events
     k_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -544,10 +550,17 @@ def main():
         h_in = [bufs[a].cpu().pin_memory() for a in range(n_up)]
         h_out = [torch.empty_like(h_in[0]).pin_memory() for _ in range(n_down)]
         pipelined = not attached and args.e2e_lanes > 1
+
+        def make_lane_stencil():
+            h = Stencil(wl["kind"], dims, wl["dtype"], variant=args.variant)
+            if args.fusion is not None:
+                h.set_fusion(args.fusion)
+            return h
+
         if pipelined:
             lanes = [(st, bufs, h_out, stream)]
             for _ in range(args.e2e_lanes - 1):
-                lanes.append((Stencil(wl["kind"], dims, wl["dtype"], variant=args.variant),
+                lanes.append((make_lane_stencil(),
                               [torch.empty_like(b) for b in bufs],
                               [torch.empty_like(h_in[0]).pin_memory() for _ in range(n_down)],
                               torch.cuda.Stream()))
@@ -621,7 +634,10 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "alg_bytes_per_launch": alg_bytes, "avg_launch_us": avg_launch_s * 1e6,
                          "kernel_only_us": k_med * 1e3,
-                         "kernel_only_frac": alg_bytes / (k_med / 1e3) / 1e9 / peak},
+                         "kernel_only_frac": alg_bytes / (k_med / 1e3) / 1e9 / peak,
+                         # throughput against the one-sweep-per-HBM-pass roofline: > 1 when
+                         # a launch applies several sweeps per pass (frac x sweeps_per_launch)
+                         "one_sweep_equiv": achieved * spl / peak},
             "clocks": clocks,
             "variants": {k: round(v, 2) for k, v in variants.items()},
             "e2e": e2e,

@@ -49,6 +49,9 @@ typedef struct stencil_s* stencil_t;
  *  ST_JACOBI2D5     in -> out, r=1   Listing 5 without the c2 term      coeffs (c0,c1)       default (0, 1/4)
  *  ST_JACOBI2D9     in -> out, r=1   Listing 5       coeffs (c0,c1,c2)    default (1/4,1/8,1/16)
  *  ST_GAUSSBLUR5X5  in -> out, r=2   Table 1 gaussblur, 25 loads        25 weights w[dj][di] default binomial/256
+ *                   (rank-1 weights are factored at create, w = u v^T: the
+ *                   register-cache kernels then run a 5-tap row pass and a
+ *                   5-tap column pass, equal to the 25-term sum up to rounding)
  *  ST_GAMEOFLIFE    in -> out, r=1   Table 1 gameoflife, int32 B3/S23   none
  *                   (cells are Life states 0 / 1; the streaming multi-sweep
  *                   kernel packs four cells per register and reads a cell as
@@ -138,16 +141,17 @@ int stencil_get_variant(stencil_t h, int* variant);
  *   0 (default) auto: grids that sit in L2 (<= 8 MiB per buffer) run the
  *                     on-chip kernels (per-launch latency bounds those runs);
  *                     larger jacobi2d5 / gameoflife grids run the streaming
- *                     three-sweep register-cache kernel, jacobi2d9 the
- *                     two-sweep one (one HBM pass per two or three sweeps:
- *                     the single-sweep kernel is HBM-bound); gaussblur keeps
- *                     one sweep per launch (issue-bound at two sweeps per
- *                     pass: no gain)
+ *                     three-sweep register-cache kernel, jacobi2d9 and
+ *                     gaussblur with separable (rank-1) weights — the default
+ *                     binomial — the two-sweep one (one HBM pass per two or
+ *                     three sweeps: the single-sweep kernel is HBM-bound); a
+ *                     gaussblur with non-separable weights keeps one sweep per
+ *                     launch (issue-bound at two sweeps per pass: no gain)
  *   1           never fuse (one sweep per launch)
  *   2           the streaming kernel with exactly two sweeps per launch
  *   3           the streaming kernel with exactly three sweeps per launch
- *               (jacobi2d5 / jacobi2d9 / gameoflife; ST_EUNSUPPORTED for
- *               gaussblur5x5)
+ *               (jacobi2d5 / jacobi2d9 / gameoflife / separable gaussblur5x5;
+ *               ST_EUNSUPPORTED for gaussblur5x5 with non-separable weights)
  *   -S (S >= 2) the shared-memory tile kernel, at most S sweeps per launch
  * A run whose sweep count is not a multiple of the streaming depth runs the
  * remainder as single sweeps first.  Anything else: ST_EARG.  Only the

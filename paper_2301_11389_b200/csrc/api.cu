@@ -2,6 +2,7 @@
 // sm_100a kernels, Dirichlet ring copy, CUDA-graph capture of stencil_run,
 // host-buffer end-to-end entry point.  Multi-GPU plumbing is in dist.cu.
 #include <cstdio>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -107,6 +108,34 @@ int stb200::kernel_setup(const void* func, int device, size_t smem, int threads)
 static size_t dtype_size(int dt) { return dt == ST_F64 ? 8 : 4; }
 
 // ------------------------------------------------------------- lifecycle
+// gaussblur5x5: if the 25 weights are rank 1 (w[dj][di] = u[dj] * v[di]
+// within 1e-12 of the largest weight, e.g. the default binomial), store
+// (u, v) for the separable kernels (k2d.cuh OpGauss5Sep).  Pivot: the
+// largest |w|; u = its column, v = its row / pivot.  STB200_GAUSS_FULL=1
+// keeps the 25-tap form (A/B experiments).
+static void gauss_factor(stencil_s* h) {
+    static const int full = getenv("STB200_GAUSS_FULL") ? atoi(getenv("STB200_GAUSS_FULL")) : 0;
+    const double* w = h->coeffs;
+    int pr = 0, pc = 0;
+    double m = 0.0;
+    for (int t = 0; t < 25; ++t)
+        if (fabs(w[t]) > m) { m = fabs(w[t]); pr = t / 5; pc = t % 5; }
+    h->gsep = false;
+    if (full || m == 0.0) return;
+    double u[5], v[5];
+    for (int d = 0; d < 5; ++d) {
+        u[d] = w[d * 5 + pc];
+        v[d] = w[pr * 5 + d] / w[pr * 5 + pc];
+    }
+    for (int t = 0; t < 25; ++t)
+        if (fabs(u[t / 5] * v[t % 5] - w[t]) > 1e-12 * m) return;
+    for (int d = 0; d < 5; ++d) {
+        h->gsep_c[d] = u[d];
+        h->gsep_c[5 + d] = v[d];
+    }
+    h->gsep = true;
+}
+
 extern "C" int stencil_create(stencil_t* out, int kind, int ndims, const int64_t* dims,
                               int dtype, const double* coeffs, int ncoeffs) {
     if (!out || !dims) return set_error(ST_EARG, "null argument");
@@ -140,6 +169,7 @@ extern "C" int stencil_create(stencil_t* out, int kind, int ndims, const int64_t
     if (ncoeffs) memcpy(h->coeffs, coeffs, sizeof(double) * ncoeffs);
     else default_coeffs(kind, h->coeffs);
     h->variant = ST_SHUFFLE;
+    if (kind == ST_GAUSSBLUR5X5) gauss_factor(h);
     if (cudaGetDevice(&h->device) != cudaSuccess) {
         delete h;
         return set_error(ST_ECUDA, "cudaGetDevice failed (no CUDA device?)");
@@ -172,8 +202,8 @@ extern "C" int stencil_set_fusion(stencil_t h, int sweeps_per_launch) {
     if (sweeps_per_launch < -64 || sweeps_per_launch > 3 || sweeps_per_launch == -1)
         return set_error(ST_EARG, "bad fusion setting %d (0 auto, 1 off, 2 / 3 streaming, -S tile)",
                          sweeps_per_launch);
-    if (sweeps_per_launch == 3 && h->k->kind == ST_GAUSSBLUR5X5)
-        return set_error(ST_EUNSUPPORTED, "gaussblur5x5 has no three-sweep streaming kernel");
+    if (sweeps_per_launch == 3 && h->k->kind == ST_GAUSSBLUR5X5 && !h->gsep)
+        return set_error(ST_EUNSUPPORTED, "gaussblur5x5 with non-separable weights has no three-sweep streaming kernel");
     h->fusion = sweeps_per_launch;
     for (auto& g : h->graphs)          // cached graphs encode the old schedule
         if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -378,7 +408,11 @@ static int pair_fusion(const stencil_s* h, int n_iters) {
     if (!fusable(h) || n_iters < 2) return 0;
     static const int env_nsw = getenv("STB200_2D_NSW") ? atoi(getenv("STB200_2D_NSW")) : 0;
     const int k = h->k->kind;
-    const bool cheap = k == ST_JACOBI2D5 || k == ST_JACOBI2D9 || k == ST_GAMEOFLIFE;
+    // gaussblur with separable (rank-1) weights: two sweeps per launch
+    // (OpGauss5Sep, 10 FMA per point: 8192^2 772 -> 1264 Gpt/s; three run
+    // slower, the 25-tap form is issue-bound at two)
+    const bool cheap = k == ST_JACOBI2D5 || k == ST_JACOBI2D9 || k == ST_GAMEOFLIFE ||
+                       (k == ST_GAUSSBLUR5X5 && h->gsep);
     // three sweeps per launch for jacobi2d5 (measured: 32768^2 fp32 1595 ->
     // 1792 Gpt/s SHUFFLE, fp64 +8%); jacobi2d9 runs slower at three (issue),
     // gaussblur has no three-sweep kernel

@@ -11,6 +11,12 @@
 
 namespace stb200 {
 
+// coefficient t of Op: the factored gaussblur weights for the separable op
+template <class Op>
+static double op_coeff(const stencil_s* h, int t) {
+    return IsSep<Op>::value ? h->gsep_c[t] : h->coeffs[t];
+}
+
 static int sm_count(int device) {
     static int cached[64] = {0};
     if (device < 0 || device >= 64) return 148;
@@ -54,7 +60,7 @@ static cudaError_t launch_k2d(const stencil_s* h, const void* in, void* out, cud
     const int64_t nstrips = (rows + H - 1) / H;
     if (nstrips > 65535) return cudaErrorInvalidConfiguration;
     Coeffs<T, Op::NC> c{};
-    for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)h->coeffs[t];
+    for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)op_coeff<Op>(h, t);
     PeerOut<T> peer;
     peer.lo = (T*)h->peer_lo;
     peer.hi = (T*)h->peer_hi;
@@ -126,6 +132,9 @@ cudaError_t dispatch_2d(stencil_s* h, const void* const* in, void* const* out, c
         return f64 ? launch_var<OpJacobi2D9, double>(h, in[0], out[0], s, a, b)
                    : launch_var<OpJacobi2D9, float>(h, in[0], out[0], s, a, b);
     case ST_GAUSSBLUR5X5:
+        if (h->gsep)
+            return f64 ? launch_var<OpGauss5Sep, double>(h, in[0], out[0], s, a, b)
+                       : launch_var<OpGauss5Sep, float>(h, in[0], out[0], s, a, b);
         return f64 ? launch_var<OpGauss5, double>(h, in[0], out[0], s, a, b)
                    : launch_var<OpGauss5, float>(h, in[0], out[0], s, a, b);
     case ST_GAMEOFLIFE:
@@ -151,7 +160,7 @@ static cudaError_t launch_tb(const stencil_s* h, const void* in, void* out, cuda
     const dim3 grid((unsigned)((nx - 2 * R + kTbTileX - 1) / kTbTileX),
                     (unsigned)((ny - 2 * R + kTbTileY - 1) / kTbTileY));
     Coeffs<T, Op::NC> c{};
-    for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)h->coeffs[t];
+    for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)op_coeff<Op>(h, t);
     ktb2d<Op, T><<<grid, kTbThreads, smem, s>>>((const T*)in, (T*)out, (int)nx, (int)ny, S, c);
     return cudaGetLastError();
 }
@@ -180,7 +189,7 @@ static cudaError_t launch_k2d2(const stencil_s* h, const void* in, void* out, cu
     const int64_t nstrips = (rows + H - 1) / H;
     if (nstrips > 65535 || ny > INT32_MAX) return cudaErrorInvalidConfiguration;
     Coeffs<T, Op::NC> c{};
-    for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)h->coeffs[t];
+    for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)op_coeff<Op>(h, t);
     kern<<<dim3((unsigned)gx, (unsigned)nstrips), k2d_threads(), smem, s>>>(
         (const T*)in, (T*)out, nx, (int)ny, (int)y_lo, (int)y_hi, (int)H, c);
     return cudaGetLastError();
@@ -198,7 +207,7 @@ static cudaError_t launch_tbr(const stencil_s* h, const void* in, void* out, cud
     kernel_setup((const void*)kern, h->device, smem, kTbrWarps * 32);
     const dim3 grid((unsigned)((nx - 2 * R + ow - 1) / ow), (unsigned)((ny - 2 * R + oh - 1) / oh));
     Coeffs<T, Op::NC> c{};
-    for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)h->coeffs[t];
+    for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)op_coeff<Op>(h, t);
     kern<<<grid, kTbrWarps * 32, smem, s>>>((const T*)in, (T*)out, (int)nx, (int)ny, S, c);
     return cudaGetLastError();
 }
@@ -265,6 +274,9 @@ cudaError_t dispatch_2d_pair(stencil_s* h, const void* in, void* out, cudaStream
         return f64 ? pair_op<OpJacobi2D9<double>, double>(h, in, out, s, nsw)
                    : pair_op<OpJacobi2D9<float>, float>(h, in, out, s, nsw);
     case ST_GAUSSBLUR5X5:   // two sweeps only (issue-bound already at two)
+        if (h->gsep)   // separable: two or three sweeps per launch
+            return f64 ? pair_op<OpGauss5Sep<double>, double>(h, in, out, s, nsw)
+                       : pair_op<OpGauss5Sep<float>, float>(h, in, out, s, nsw);
         if (h->variant == ST_PLAIN)
             return f64 ? launch_k2d2<OpGauss5<double>, double, VAR_PLAIN, 2>(h, in, out, s)
                        : launch_k2d2<OpGauss5<float>, float, VAR_PLAIN, 2>(h, in, out, s);
@@ -297,6 +309,9 @@ cudaError_t dispatch_2d_fused(stencil_s* h, const void* in, void* out, cudaStrea
         return f64 ? launch_fused<OpJacobi2D9<double>, double>(h, in, out, s, S)
                    : launch_fused<OpJacobi2D9<float>, float>(h, in, out, s, S);
     case ST_GAUSSBLUR5X5:
+        if (h->gsep)
+            return f64 ? launch_fused<OpGauss5Sep<double>, double>(h, in, out, s, S)
+                       : launch_fused<OpGauss5Sep<float>, float>(h, in, out, s, S);
         return f64 ? launch_fused<OpGauss5<double>, double>(h, in, out, s, S)
                    : launch_fused<OpGauss5<float>, float>(h, in, out, s, S);
     case ST_GAMEOFLIFE: return launch_fused<OpLife, int>(h, in, out, s, S);

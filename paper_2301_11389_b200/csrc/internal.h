@@ -46,6 +46,10 @@ struct stencil_s {
     void* peer_hi = nullptr;
     int64_t peer_lo_end = 0, peer_hi_begin = 0, peer_d_lo = 0, peer_d_hi = 0;
     int rank = 0, nranks = 1;
+    // gaussblur5x5 weights factored as w[dj][di] = u[dj] * v[di] (api.cu, at
+    // create): the separable kernels' coefficients (u[0..4], v[0..4])
+    bool gsep = false;
+    double gsep_c[10] = {0};
 };
 
 namespace stb200 {

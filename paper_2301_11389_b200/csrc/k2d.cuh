@@ -120,6 +120,88 @@ template <typename T> struct OpGauss5 {
     }
 };
 
+// gaussblur5x5 with rank-1 weights w[dj][di] = u[dj] * v[di] (the default
+// binomial [1,4,6,4,1]^T [1,4,6,4,1] / 256; api.cu factors the 25 weights at
+// create).  Coefficients c = (u[0..4], v[0..4]).  The streaming kernels (k2d,
+// k2d2) apply a row pass to every staged row once,
+//   h[p] = v0 x[p-2] + v1 x[p-1] + ... + v4 x[p+2]      (one FMA chain),
+// keep the row-pass values in the register y-window, and finish with a
+// column pass  out = u0 h[y-2] + ... + u4 h[y+2]: 10 FMA per point instead of
+// 25.  point() evaluates the same two chains from a raw
+// window (30 FMA: the tile / register kernels ktb2d, ktb2r), so every kernel
+// family gives the same bits.  The result differs from the 25-term oracle
+// order by rounding only (DESIGN.md §7 tolerance).
+template <typename T> struct OpGauss5Sep {
+    static constexpr int R = 2, NC = 10;
+    // fp32: two adjacent points per packed FFMA2 (the same per-point chains;
+    // an operand pair starting at an odd element would need two moves, so
+    // those taps are two scalar FFMAs, as in OpGauss5::point2)
+    static constexpr bool kPaired = std::is_same<T, float>::value;
+    template <int V>
+    __device__ __forceinline__ static void rowpass(const T* x, T* h, const Coeffs<T, NC>& c) {
+        if constexpr (kPaired && V % 2 == 0) {
+#pragma unroll
+            for (int p = 0; p < V; p += 2) {
+                float2 a = __fmul2_rn(make_float2(c.c[5], c.c[5]), make_float2(x[p], x[p + 1]));
+#pragma unroll
+                for (int d = 1; d < 5; ++d) {
+                    if (((p + d) & 1) == 0) {
+                        a = __ffma2_rn(make_float2(c.c[5 + d], c.c[5 + d]), make_float2(x[p + d], x[p + d + 1]), a);
+                    } else {
+                        a.x = fmaf(c.c[5 + d], x[p + d], a.x);
+                        a.y = fmaf(c.c[5 + d], x[p + d + 1], a.y);
+                    }
+                }
+                h[p] = a.x;
+                h[p + 1] = a.y;
+            }
+        } else {
+#pragma unroll
+            for (int p = 0; p < V; ++p) {
+                T a = c.c[5] * x[p];
+#pragma unroll
+                for (int d = 1; d < 5; ++d) a = fma(c.c[5 + d], x[p + d], a);
+                h[p] = a;
+            }
+        }
+    }
+    // column pass over a window of row-pass values (centre slots e = p + R)
+    template <class Wn>
+    __device__ __forceinline__ static T colpoint(const Wn& w, int p, const Coeffs<T, NC>& c) {
+        const int e = p + R;
+        T acc = c.c[0] * w(-2, e);
+#pragma unroll
+        for (int d = 1; d < 5; ++d) acc = fma(c.c[d], w(d - 2, e), acc);
+        return acc;
+    }
+    // points p, p+1 (p even: the centre slots p+R, p+R+1 are an aligned pair)
+    template <class Wn>
+    __device__ __forceinline__ static float2 colpoint2(const Wn& w, int p, const Coeffs<T, NC>& c) {
+        const int e = p + R;
+        float2 acc = __fmul2_rn(make_float2(c.c[0], c.c[0]), make_float2(w(-2, e), w(-2, e + 1)));
+#pragma unroll
+        for (int d = 1; d < 5; ++d)
+            acc = __ffma2_rn(make_float2(c.c[d], c.c[d]), make_float2(w(d - 2, e), w(d - 2, e + 1)), acc);
+        return acc;
+    }
+    // the same value from a window of raw rows
+    template <class Wn>
+    __device__ __forceinline__ static T point(const Wn& w, int p, const Coeffs<T, NC>& c) {
+        auto hrow = [&](int dj) {
+            T a = c.c[5] * w(dj, p);
+#pragma unroll
+            for (int d = 1; d < 5; ++d) a = fma(c.c[5 + d], w(dj, p + d), a);
+            return a;
+        };
+        T acc = c.c[0] * hrow(-2);
+#pragma unroll
+        for (int d = 1; d < 5; ++d) acc = fma(c.c[d], hrow(d - 2), acc);
+        return acc;
+    }
+};
+template <class Op, class = void> struct IsSep : std::false_type {};
+template <typename T> struct IsSep<OpGauss5Sep<T>> : std::true_type {};
+
 template <class Op, class = void> struct HasPaired : std::false_type {};
 template <class Op> struct HasPaired<Op, std::enable_if_t<Op::kPaired>> : std::true_type {};
 
@@ -222,10 +304,14 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
     T win[NW][W];
 
     const bool lane0 = lane == 0, lane31 = lane == 31;
+    Coeffs<T, Op::NC> cr;                                  // coefficients held in registers
+#pragma unroll
+    for (int t = 0; t < Op::NC; ++t) cr.c[t] = c.c[t];
     // S2..S4: strip row r -> register window row dst
     const uint32_t rt_zero = (uint32_t)((uint64_t)nx >> 48);   // 0 at run time, unknown to the compiler
     auto consume = [&](unsigned r, T* dst) {
         const unsigned s = r & (S - 1);
+        if (STB200_REL_LAG) ring_release_lagged<S>(empty, r);   // rows before r (pipe.cuh)
         mbar_wait(&full[s], (r >> LOG2S) & 1u);
         const T* row = ring + s * WS;
         T v[V];
@@ -256,7 +342,13 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
         // register of every LDS issued above feeds the (zero) dependency
         uint32_t dep = bits32(dst[0]) ^ bits32(dst[R - 1]) ^ bits32(dst[R + V]) ^ bits32(dst[R + V + R - 1]) ^
                        bits32(dst[R]) ^ bits32(dst[R + V - 1]);
-        mbar_release(&empty[s], dep & rt_zero);                           // this lane is done with stage s
+        if (!STB200_REL_LAG) mbar_release(&empty[s], dep & rt_zero);                           // this lane is done with stage s
+        if constexpr (IsSep<Op>::value) {                  // separable: the row pass, once per row
+            T hv[V];
+            Op::template rowpass<V>(dst, hv, cr);
+#pragma unroll
+            for (int k = 0; k < V; ++k) dst[R + k] = hv[k];
+        }
     };
 
     // S7 masks: whole-vector store for lanes fully inside the interior, else
@@ -266,9 +358,6 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
     bool el_store[V];
 #pragma unroll
     for (int p = 0; p < V; ++p) el_store[p] = !vec_store && own && xl + p >= R && xl + p < nx - R;
-    Coeffs<T, Op::NC> cr;                                  // coefficients held in registers
-#pragma unroll
-    for (int t = 0; t < Op::NC; ++t) cr.c[t] = c.c[t];
 
 #pragma unroll
     for (int r = 0; r < 2 * R; ++r) consume((unsigned)r, win[r]);
@@ -279,7 +368,17 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
         auto emit = [&](int u, int yrow) {
             T o[V];
             const Win<T, NW, W, R> w{win, u};
-            if constexpr (HasPaired<Op>::value) {                       // S6
+            if constexpr (IsSep<Op>::value && HasPaired<Op>::value) {            // S6, separable, FFMA2
+#pragma unroll
+                for (int p = 0; p < V; p += 2) {
+                    const float2 r = Op::colpoint2(w, p, cr);
+                    o[p] = r.x;
+                    o[p + 1] = r.y;
+                }
+            } else if constexpr (IsSep<Op>::value) {                    // S6, separable
+#pragma unroll
+                for (int p = 0; p < V; ++p) o[p] = Op::colpoint(w, p, cr);
+            } else if constexpr (HasPaired<Op>::value) {                // S6
 #pragma unroll
                 for (int p = 0; p < V; p += 2) {
                     const float2 r = Op::point2(w, p, cr);

@@ -32,6 +32,10 @@
 
 namespace stb200 {
 
+// minimum resident CTAs per SM (register cap), build knob for A/Bs
+#ifndef STB200_2D2_MINB
+#define STB200_2D2_MINB 1
+#endif
 #ifndef STB200_2D2_FBSEL
 #define STB200_2D2_FBSEL 1        // SHUFFLE fallback as one load + selects (0: predicated asm loads)
 #endif
@@ -42,13 +46,13 @@ constexpr int k2d2_row_elems() { return kWarps2D * k2d2_txo<T, NSW>() + 2 * NSW 
 template <typename T, int NSW = 2>
 constexpr size_t k2d2_smem_bytes() {
     return (size_t)kStages2D * (k2d2_row_elems<T, NSW>() * sizeof(T) + 2 * sizeof(uint64_t)) +
-           (size_t)kWarps2D * (32 + 2) * vlen<T>() * sizeof(T);        // PLAIN: per-warp sweep row
+           (size_t)(NSW - 1) * kWarps2D * (32 + 2) * vlen<T>() * sizeof(T);   // PLAIN: per-warp, per-level sweep row
 }
 
 // Grid: x = ceil(nx / (kWarps2D * TXO)), y = strips of H output rows
 // covering [y_lo, y_hi) (R <= y_lo, y_hi <= ny - R).  NSW sweeps per launch.
 template <class Op, typename T, int VARIANT, int NSW = 2>
-__global__ void __launch_bounds__(k2d_threads())
+__global__ void __launch_bounds__(k2d_threads(), STB200_2D2_MINB)
 k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo, int y_hi, int H,
      Coeffs<T, Op::NC> c) {
     static_assert(NSW == 2 || NSW == 3, "two or three sweeps per launch");
@@ -66,7 +70,7 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
     T* ring = reinterpret_cast<T*>(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * WS * sizeof(T));
     uint64_t* empty = full + S;
-    T* s1row = reinterpret_cast<T*>(empty + S);            // PLAIN: [kWarps2D][32V + 2V]
+    T* s1row = reinterpret_cast<T*>(empty + S);            // PLAIN: [NSW-1][kWarps2D][32V + 2V]
 
     const int warp = threadIdx.x >> 5;
     const int lane = lane_id();
@@ -119,9 +123,31 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
     const bool lane0 = lane == 0, lane31 = lane == 31;
     T wl[NSW][NW][W];                                      // level 0: input rows; k: sweep-k rows
 
+    Coeffs<T, Op::NC> cr;
+#pragma unroll
+    for (int t = 0; t < Op::NC; ++t) cr.c[t] = c.c[t];
+    // separable kinds (OpGauss5Sep): a window row keeps the row-pass values
+    // in its centre slots and the raw centre values in its halo slots
+    // (needed for the held boundary ring); slot of raw element p:
+    auto raw_slot = [](int p) { return p < R ? p : V + p; };
+    auto sep_row = [&](T* d) {
+        if constexpr (IsSep<Op>::value) {
+            static_assert(V <= 2 * R, "raw centre values must fit the halo slots");
+            T hv[V], rv[V];
+#pragma unroll
+            for (int k = 0; k < V; ++k) rv[k] = d[R + k];
+            Op::template rowpass<V>(d, hv, cr);
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                d[R + k] = hv[k];
+                d[raw_slot(k)] = rv[k];
+            }
+        }
+    };
     const uint32_t rt_zero = (uint32_t)((uint64_t)nx >> 48);   // 0 at run time, unknown to the compiler
     auto consume = [&](unsigned r, T* dst) {
         const unsigned s = r & (S - 1);
+        if (STB200_REL_LAG) ring_release_lagged<S>(empty, r);   // rows before r (pipe.cuh)
         mbar_wait(&full[s], (r >> LOG2S) & 1u);
         const T* row = ring + s * WS;
         T v[V];
@@ -166,7 +192,8 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
         // register of every LDS issued above feeds the (zero) dependency
         uint32_t dep = bits32(dst[0]) ^ bits32(dst[R - 1]) ^ bits32(dst[R + V]) ^ bits32(dst[R + V + R - 1]) ^
                        bits32(dst[R]) ^ bits32(dst[R + V - 1]);
-        mbar_release(&empty[s], dep & rt_zero);
+        if (!STB200_REL_LAG) mbar_release(&empty[s], dep & rt_zero);
+        sep_row(dst);
     };
 
     // per-element masks: interior columns (sweep 1 computes, else keeps the
@@ -179,13 +206,24 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
     bool el_store[V];
 #pragma unroll
     for (int p = 0; p < V; ++p) el_store[p] = !vec_store && own && xin[p];
-    Coeffs<T, Op::NC> cr;
-#pragma unroll
-    for (int t = 0; t < Op::NC; ++t) cr.c[t] = c.c[t];
-    T* srow = s1row + warp * (32 + 2) * V + V;             // PLAIN staging: element e <-> column xs + e
+    // PLAIN staging of sweep level k (1..NSW-1): element e <-> column xs + e.
+    // One row per level: with a single row shared by the levels, the
+    // three-sweep PLAIN kernel gave run-to-run differences (tools/flake_hunt.py,
+    // jacobi2d5 32768^2: 7 of 8 repeats) although __syncwarp orders each reuse.
+    auto srow_of = [&](int k) { return s1row + ((k - 1) * kWarps2D + warp) * (32 + 2) * V + V; };
 
     auto point_row = [&](const auto& w, T* o) {
-        if constexpr (HasPaired<Op>::value) {
+        if constexpr (IsSep<Op>::value && HasPaired<Op>::value) {
+#pragma unroll
+            for (int p = 0; p < V; p += 2) {
+                const float2 r = Op::colpoint2(w, p, cr);
+                o[p] = r.x;
+                o[p + 1] = r.y;
+            }
+        } else if constexpr (IsSep<Op>::value) {
+#pragma unroll
+            for (int p = 0; p < V; ++p) o[p] = Op::colpoint(w, p, cr);
+        } else if constexpr (HasPaired<Op>::value) {
 #pragma unroll
             for (int p = 0; p < V; p += 2) {
                 const float2 r = Op::point2(w, p, cr);
@@ -199,7 +237,7 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
     };
 
     // the x halo of a sweep row from the neighbour lanes
-    auto halo = [&](const T* v, T* d) {
+    auto halo = [&](const T* v, T* d, int lev) {
 #pragma unroll
         for (int k = 0; k < V; ++k) d[R + k] = v[k];
         if constexpr (VARIANT == VAR_SHUFFLE) {
@@ -208,6 +246,7 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
 #pragma unroll
             for (int k = 0; k < R; ++k) d[R + V + k] = shfl_down(v[k], 1);
         } else {
+            T* srow = srow_of(lev);
             __syncwarp();                                  // previous row's reads are done
             stg_vec(srow + lane * V, v);                   // STS.128 (generic store to smem)
             __syncwarp();
@@ -242,10 +281,14 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
                 if constexpr (EDGE) {
                     const bool yint = yk >= R && yk < ny - R;
 #pragma unroll
-                    for (int p = 0; p < V; ++p)                 // boundary ring: held value
-                        if (!(yint && xin[p])) v[p] = wl[k - 1][(ph + R) % NW][R + p];
+                    for (int p = 0; p < V; ++p) {               // boundary ring: held value
+                        const T held = IsSep<Op>::value ? wl[k - 1][(ph + R) % NW][raw_slot(p)]
+                                                        : wl[k - 1][(ph + R) % NW][R + p];
+                        if (!(yint && xin[p])) v[p] = held;
+                    }
                 }
-                halo(v, wl[k][u % NW]);
+                halo(v, wl[k][u % NW], k);
+                sep_row(wl[k][u % NW]);
             } else {
                 T* op = out + (int64_t)yk * nx + xl;
                 if constexpr (EDGE) {

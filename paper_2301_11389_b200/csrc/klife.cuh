@@ -122,6 +122,7 @@ k2dlife(const int* __restrict__ in, int* __restrict__ out, int64_t nx, int ny, i
     const uint32_t rt_zero = (uint32_t)((uint64_t)nx >> 48);
     auto consume = [&](unsigned r, int slot) {
         const unsigned s = r & (S - 1);
+        if (STB200_REL_LAG) ring_release_lagged<S>(empty, r);   // rows before r (pipe.cuh)
         mbar_wait(&full[s], (r >> LOG2S) & 1u);
         const int* row = ring + s * WS;
         int v[V];
@@ -146,7 +147,7 @@ k2dlife(const int* __restrict__ in, int* __restrict__ out, int64_t nx, int ny, i
         wp[0][slot] = p;
         wh[0][slot] = life_hsum(l, p, rr);
         // release after the loads completed (pipe.cuh mbar_release)
-        mbar_release(&empty[s], (bits32(v[0]) ^ bits32(v[3]) ^ l ^ rr) & rt_zero);
+        if (!STB200_REL_LAG) mbar_release(&empty[s], (bits32(v[0]) ^ bits32(v[3]) ^ l ^ rr) & rt_zero);
     };
 
     // interior columns of the lane as a byte mask (EDGE path: ring cells keep their value)

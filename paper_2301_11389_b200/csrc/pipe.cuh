@@ -42,13 +42,40 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // loads from it were ISSUED.  Measured on B200: a plain
 // arrive issued behind in-flight LDS lets the producer's next bulk copy
 // overwrite the stage before those loads read it (PLAIN gaussblur 8192^2
-// x100 differed run to run).  `dep` is 0 at run time but is computed from
-// the loaded registers, so the arrive waits for the loads to complete.
-// STB200_REL (build knob): 2 = data dependency (default), 1 =
-// fence.proxy.async + arrive, 0 = plain arrive (the racy form, A/B only).
+// x100 differed run to run).  The release is ordered by a cross-proxy fence
+// (fence.proxy.async: the thread's generic-proxy reads of the stage before
+// the async-proxy writes the producer issues after this arrival).
+// STB200_REL (build knob): 1 = fence.proxy.async + arrive (default); 2 =
+// the round-1 data-dependency form (`dep`, 0 at run time but computed from
+// the loaded registers, added to the barrier address) — it was NOT enough:
+// jacobi2d5 32768^2 three-sweep PLAIN and jacobi2d9 two-sweep runs still
+// differed run to run (tools/flake_hunt.py, round 2), the fenced form is
+// clean; 0 = plain arrive (racy, A/B only).
 #ifndef STB200_REL
-#define STB200_REL 2
+#define STB200_REL 1
 #endif
+// Streaming row rings (k2d, k2d2, klife): the stage of row r is released at
+// the START of consume(r + 1), fenced — by then row r's loads have been
+// consumed by the arithmetic, so the proxy fence has nothing left to wait
+// for (releasing right after the loads, fenced, cost 6-10% on the PLAIN
+// variants).  0 = release right after the loads (STB200_REL form).
+#ifndef STB200_REL_LAG
+#define STB200_REL_LAG 1
+#endif
+// ... in batches of STB200_REL_BATCH rows per fence (consume(r), r % B == 0,
+// releases rows r-B .. r-1 behind one fence)
+#ifndef STB200_REL_BATCH
+#define STB200_REL_BATCH 1
+#endif
+template <unsigned S>
+__device__ __forceinline__ void ring_release_lagged(uint64_t* empty, unsigned r) {
+    constexpr unsigned B = STB200_REL_BATCH;
+    if (r == 0 || r % B != 0) return;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+    for (unsigned q = r - B; q < r; ++q)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[q & (S - 1)])) : "memory");
+}
 __device__ __forceinline__ void mbar_release(uint64_t* bar, uint32_t dep) {
     uint32_t a = smem_u32(bar);
     if (STB200_REL == 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -136,9 +136,17 @@ def test_fusion_settings_validated():
         with pytest.raises(StencilError) as e:
             st.set_fusion(bad)
         assert e.value.code == -1
-    g = Stencil("gaussblur5x5", (4100, 600), "f32")
+    # three streaming sweeps need separable weights (OpGauss5Sep); the default
+    # binomial is separable and runs two sweeps per launch automatically
+    w = np.arange(25, dtype=np.float64) / 300.0           # rank 2: not separable
+    g = Stencil("gaussblur5x5", (4100, 600), "f32", coeffs=w)
     with pytest.raises(StencilError) as e:
         g.set_fusion(3)
     assert e.value.code == -2
+    assert g.info()["sweeps_per_launch"] == 1              # auto: the 25-tap form stays single-sweep
     g.set_fusion(2)
     assert g.info()["sweeps_per_launch"] == 2
+    b = Stencil("gaussblur5x5", (4100, 600), "f32")       # binomial: separable
+    assert b.info()["sweeps_per_launch"] == 2
+    b.set_fusion(3)
+    assert b.info()["sweeps_per_launch"] == 3

@@ -31,7 +31,10 @@ def test_default_line_contract():
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] == pytest.approx(r["achieved"] / r["peak"])
     assert d["e2e"]["h2d_bytes_per_step"] == 8192 * 8192 * 4 and d["e2e"]["value"] > 0
-    assert d["gpu_launches"] >= 3 * 100
+    # 100 sweeps per step at sweeps_per_launch sweeps per launch (+ the ring copy)
+    spl = d["config"]["sweeps_per_launch"]
+    assert spl in (1, 2) and d["gpu_launches"] >= 3 * (100 // spl)
+    assert r["one_sweep_equiv"] == pytest.approx(r["frac"] * spl)
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["config"]["kind"] == "gaussblur5x5" and d["config"]["dims"] == [8192, 8192]
 

@@ -102,7 +102,8 @@ def _rank(rank, world, port, kind, dtype, dims, n_iters, q, transport="host", ru
             st.p2p_register(bufs, _allgather)
         for _ in range(runs - 1):          # consecutive runs on the same buffers (epochs carry over)
             i = st.run(bufs, n_iters)
-            assert i == n_iters % 2          # attached runs are single sweeps: no rotation needed
+            if n_bufs == 2:                  # attached runs are single sweeps: no rotation needed
+                assert i == n_iters % 2
         idx = st.run(bufs, n_iters)
         torch.cuda.synchronize()
         nres = n_out if n_bufs > 3 else 1

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--shape", default="", help="nz,ny,nx for 3-D kinds (numpy order)")
     ap.add_argument("--dtype", default="f32")
+    ap.add_argument("--variants", default="plain,shuffle")
     a = ap.parse_args()
     shape = tuple(int(v) for v in a.shape.split(",")) if a.shape else (a.n, a.n)
     dims = shape[::-1]
@@ -39,7 +40,7 @@ def main():
     other = torch.from_numpy(inputs.generate_np((130, 258, 256), "f32", 7)).cuda()
     oth = Stencil("laplacian3d7", (256, 258, 130), "f32")
     bad = 0
-    for var in ("plain", "shuffle"):
+    for var in a.variants.split(","):
         ref = None
         for r in range(a.reps):
             st = Stencil(a.kind, dims, a.dtype, variant=var)

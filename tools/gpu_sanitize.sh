@@ -7,5 +7,5 @@ for tool in memcheck synccheck initcheck; do
 done
 timeout 1500 compute-sanitizer --tool racecheck --racecheck-report all --print-limit 20 python tools/sanitize_run.py --quick > gpurun_out/sanitize_racecheck.txt 2>&1
 echo racecheck $?; tail -3 gpurun_out/sanitize_racecheck.txt
-timeout 600 compute-sanitizer --tool memcheck --print-limit 3 python tools/sanitize_run.py --canary > gpurun_out/sanitize_canary.txt 2>&1
+PYTORCH_NO_CUDA_MEMORY_CACHING=1 timeout 600 compute-sanitizer --tool memcheck --print-limit 3 python tools/sanitize_run.py --canary > gpurun_out/sanitize_canary.txt 2>&1
 echo canary $?; tail -3 gpurun_out/sanitize_canary.txt

@@ -20,9 +20,12 @@ ap.add_argument("--workload", default="gaussblur")
 ap.add_argument("--variant", default="shuffle")
 ap.add_argument("--launches", type=int, default=8)
 ap.add_argument("--run", action="store_true", help="one stencil_run (graph) instead of steps")
+ap.add_argument("--fusion", type=int, default=None, help="stencil_set_fusion before the run")
 a = ap.parse_args()
 wl = bench.WORKLOADS[a.workload]
 st = Stencil(wl["kind"], wl["dims"], wl["dtype"], variant=a.variant)
+if a.fusion is not None:
+    st.set_fusion(a.fusion)
 n_in, n_out, n_bufs = st.arity()
 shape = tuple(wl["dims"][::-1])
 f = [inputs.generate_torch(shape, wl["dtype"], 1, k) for k in range(n_in)]

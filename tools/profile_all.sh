@@ -5,7 +5,7 @@
 #   -> gpurun_out/ncu/${ROUND}_ncu_summary.md, traffic.json, ops_<w>_<v>.txt (dynamic opcode mix)
 #      and the .ncu-rep of KEEP for source-level reading.  Workloads ending in
 #      _pair profile one multi-sweep launch inside a stencil_run (k2d2 / k2dlife).
-W=${@:-"gaussblur jacobi2d_paper gameoflife laplacian wave13pt jacobi3d divergence gradient tricubic uxx1 whispering lapgsrb tricubic2 jacobi2d_paper_pair gameoflife_pair"}
+W=${@:-"gaussblur jacobi2d_paper gameoflife laplacian wave13pt jacobi3d divergence gradient tricubic uxx1 whispering lapgsrb tricubic2 jacobi2d_paper_pair gameoflife_pair gaussblur_pair"}
 KEEP=${KEEP:-"prof_tricubic_shuffle prof_lapgsrb_shuffle"}
 ROUND=${ROUND:-r02}
 mkdir -p gpurun_out/ncu /tmp/ncu_reps
