@@ -311,7 +311,7 @@ k2d(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int y_lo, int y_h
     const uint32_t rt_zero = (uint32_t)((uint64_t)nx >> 48);   // 0 at run time, unknown to the compiler
     auto consume = [&](unsigned r, T* dst) {
         const unsigned s = r & (S - 1);
-        if (STB200_REL_LAG) ring_release_lagged<S>(empty, r);   // rows before r (pipe.cuh)
+        if (STB200_REL_LAG) ring_release_lagged<S, VARIANT == VAR_PLAIN ? 4 : 1>(empty, r);   // rows before r (pipe.cuh)
         mbar_wait(&full[s], (r >> LOG2S) & 1u);
         const T* row = ring + s * WS;
         T v[V];

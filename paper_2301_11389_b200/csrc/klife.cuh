@@ -122,7 +122,7 @@ k2dlife(const int* __restrict__ in, int* __restrict__ out, int64_t nx, int ny, i
     const uint32_t rt_zero = (uint32_t)((uint64_t)nx >> 48);
     auto consume = [&](unsigned r, int slot) {
         const unsigned s = r & (S - 1);
-        if (STB200_REL_LAG) ring_release_lagged<S>(empty, r);   // rows before r (pipe.cuh)
+        if (STB200_REL_LAG) ring_release_lagged<S, VARIANT == VAR_PLAIN ? 4 : 1>(empty, r);   // rows before r (pipe.cuh)
         mbar_wait(&full[s], (r >> LOG2S) & 1u);
         const int* row = ring + s * WS;
         int v[V];

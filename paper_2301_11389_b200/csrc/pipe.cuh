@@ -62,14 +62,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 #ifndef STB200_REL_LAG
 #define STB200_REL_LAG 1
 #endif
-// ... in batches of STB200_REL_BATCH rows per fence (consume(r), r % B == 0,
-// releases rows r-B .. r-1 behind one fence)
+// ... in batches of B rows per fence (consume(r), r % B == 0, releases rows
+// r-B .. r-1 behind one fence).  Measured (round 2, tools/gpu_lag_ab.sh):
+// B = 4 helps the PLAIN kernels (gaussblur 1165 -> 1213, jacobi2d5 three-sweep
+// 1531 -> 1627 Gpt/s), B = 1 suits SHUFFLE (1214 / 1911 vs 1206 / 1846):
+// the kernels pass B per variant.  STB200_REL_BATCH overrides (A/B builds).
 #ifndef STB200_REL_BATCH
-#define STB200_REL_BATCH 1
+#define STB200_REL_BATCH 0
 #endif
-template <unsigned S>
+template <unsigned S, unsigned B0 = 1>
 __device__ __forceinline__ void ring_release_lagged(uint64_t* empty, unsigned r) {
-    constexpr unsigned B = STB200_REL_BATCH;
+    constexpr unsigned B = STB200_REL_BATCH > 0 ? STB200_REL_BATCH : B0;
     if (r == 0 || r % B != 0) return;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #pragma unroll
