@@ -46,6 +46,10 @@ WORKLOADS = {
                      config="BASELINE configs[0]: jacobi 2D 5-point fp32 512x512, 10 sweeps"),
     "jacobi2d_paper": dict(kind="jacobi2d5", dtype="f32", dims=(32768, 32768), iters=10,
                            config="jacobi 2D 5-point fp32 at the paper's 2-D size 32768^2 (PAPER.md:644)"),
+    "jacobi2d9": dict(kind="jacobi2d9", dtype="f32", dims=(32768, 32768), iters=10,
+                      config="jacobi 2D 9-point fp32 32768^2 (Table 1 jacobi row, box form; not a BASELINE config)"),
+    "jacobi2d_f64": dict(kind="jacobi2d5", dtype="f64", dims=(16384, 16384), iters=10,
+                         config="jacobi 2D 5-point fp64 16384^2 (not a BASELINE config)"),
     "gameoflife": dict(kind="gameoflife", dtype="i32", dims=(16384, 16384), iters=10,
                        config="BASELINE configs[3]: gameoflife int32 16384x16384"),
     "laplacian": dict(kind="laplacian3d7", dtype="f64", dims=(512, 512, 512), iters=10,
@@ -336,7 +340,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="gaussblur", choices=sorted(WORKLOADS))
-    ap.add_argument("--variant", default="shuffle", choices=["shuffle", "plain"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "shuffle", "plain"],
+                    help="auto (default): the library's ST_AUTO, the kind's measured-faster variant; "
+                         "the other variant is timed too and reported under 'variants'")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-lanes", type=int, default=4,
@@ -408,6 +414,8 @@ def main():
             dist, torch, dist_get_id)
     else:
         st = Stencil(wl["kind"], dims, wl["dtype"], variant=args.variant)
+    variant_rule = args.variant
+    args.variant = st.variant              # "auto" resolved by the library (ST_AUTO)
     if args.fusion is not None:
         st.set_fusion(args.fusion)
     info = st.info()
@@ -622,7 +630,7 @@ def main():
             "dtype": wl["dtype"], "data": "synthetic (splitmix64 seeded grids, DESIGN.md §6)",
             "config": {"workload": wl["config"], "kind": wl["kind"], "dims": dims,
                        "local_dims": list(ldims), "iters_per_step": iters,
-                       "variant": args.variant,
+                       "variant": args.variant, "variant_rule": variant_rule,
                        "parallelism": (f"slab{world}" if world > 1 else "slab1") if attached else "1gpu",
                        "transport": transport,
                        "l2": "flushed between timed steps" if flush is not None

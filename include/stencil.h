@@ -105,11 +105,15 @@ enum stencil_dtype { ST_F32 = 1, ST_F64 = 2, ST_I32 = 3 };
  *  ST_PAPER_NOLOAD:   covered loads removed (INVALID results)
  *  ST_PAPER_NOCORNER: shuffles without corner fallback (INVALID at warp edges)
  *  ST_PAPER_UNIFORM:  warp-uniform branch on completeness
- * Bit-identical to SHUFFLE/PLAIN except NOLOAD and NOCORNER. */
+ * Bit-identical to SHUFFLE/PLAIN except NOLOAD and NOCORNER.
+ *  ST_AUTO: resolved by stencil_set_variant, per kind, to whichever of
+ *           SHUFFLE / PLAIN ran faster on B200 at the kind's benchmark size
+ *           (the answer differs by kind); stencil_get_variant
+ *           then reports the resolved variant. */
 enum stencil_variant {
     ST_SHUFFLE = 0, ST_PLAIN = 1,
     ST_PAPER_ORIGINAL = 2, ST_PAPER_PTXASW = 3, ST_PAPER_NOLOAD = 4, ST_PAPER_NOCORNER = 5,
-    ST_PAPER_UNIFORM = 6
+    ST_PAPER_UNIFORM = 6, ST_AUTO = 7
 };
 
 enum stencil_status {

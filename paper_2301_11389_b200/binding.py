@@ -20,7 +20,8 @@ KINDS = {"jacobi2d5": 1, "jacobi2d9": 2, "gaussblur5x5": 3, "gameoflife": 4,
          "gradient": 9, "tricubic": 10, "tricubic2": 11, "uxx1": 12, "lapgsrb": 13, "whispering": 14}
 DTYPES = {"f32": 1, "f64": 2, "i32": 3}
 VARIANTS = {"shuffle": 0, "plain": 1, "paper_original": 2, "paper_ptxasw": 3,
-            "paper_noload": 4, "paper_nocorner": 5, "paper_uniform": 6}
+            "paper_noload": 4, "paper_nocorner": 5, "paper_uniform": 6,
+            "auto": 7}
 STATUS = {0: "ST_OK", -1: "ST_EARG", -2: "ST_EUNSUPPORTED", -3: "ST_EALIGN",
           -4: "ST_ECUDA", -5: "ST_ENCCL", -6: "ST_ESTATE"}
 
@@ -163,8 +164,12 @@ class Stencil:
 
     # -- queries
     def set_variant(self, variant: str):
+        """A variant name; "auto" resolves (in the library) to the kind's
+        measured-faster register-cache variant, reported in self.variant."""
         _check(lib().stencil_set_variant(self._h, VARIANTS[variant]), "stencil_set_variant")
-        self.variant = variant
+        v = ctypes.c_int()
+        _check(lib().stencil_get_variant(self._h, ctypes.byref(v)), "stencil_get_variant")
+        self.variant = next(n for n, i in VARIANTS.items() if i == v.value)
 
     def set_fusion(self, sweeps_per_launch: int):
         """0 auto (fuse L2-resident 2-D runs), 1 off, S >= 2 sweeps per launch."""

@@ -178,8 +178,28 @@ extern "C" int stencil_create(stencil_t* out, int kind, int ndims, const int64_t
     return ST_OK;
 }
 
+// ST_AUTO: the register-cache variant measured faster on B200 for the kind
+// (profiles/r02_bench_all.txt, one session, 10 steps at the benchmark sizes,
+// Gpt/s SHUFFLE vs PLAIN).  Within 2% either way: SHUFFLE (the paper's form).
+static int auto_variant(const stencil_s* h) {
+    switch (h->k->kind) {
+    case ST_GAUSSBLUR5X5:  // 8192^2 two sweeps per pass: 1208 vs 1358
+    case ST_GAMEOFLIFE:    // 16384^2 packed three-sweep: 1858 vs 1889
+    case ST_WAVE13PT:      // fp64 512^3: 250 vs 257
+    case ST_JACOBI3D7:     // fp32 1024^3: 697 vs 710
+    case ST_TRICUBIC:      // fp32 256^3: 165 vs 181
+    case ST_TRICUBIC2:     // 165 vs 181
+    case ST_UXX1:          // 258 vs 272
+    case ST_WHISPERING:    // 149 vs 152
+        return ST_PLAIN;
+    default:               // jacobi2d5 32768^2 2019 vs 1630, lapgsrb 571 vs 515,
+        return ST_SHUFFLE; // laplacian 367 vs 359, gradient 325 vs 320, divergence even
+    }
+}
+
 extern "C" int stencil_set_variant(stencil_t h, int variant) {
     if (!h) return set_error(ST_EARG, "null handle");
+    if (variant == ST_AUTO) variant = auto_variant(h);
     if (variant < ST_SHUFFLE || variant > ST_PAPER_UNIFORM)
         return set_error(ST_EUNSUPPORTED, "unknown variant %d", variant);
     if (variant >= ST_PAPER_ORIGINAL && h->k->kind >= ST_TRICUBIC2)

@@ -32,27 +32,51 @@
 
 namespace stb200 {
 
-// minimum resident CTAs per SM (register cap), build knob for A/Bs
-#ifndef STB200_2D2_MINB
-#define STB200_2D2_MINB 1
+#ifndef STB200_2D2_S
+#define STB200_2D2_S 16           // staged rows per CTA (ring stages); power of 2
 #endif
+constexpr int kStages2D2 = STB200_2D2_S;
+#ifndef STB200_2D2_NW
+#define STB200_2D2_NW 4           // consumer warps per CTA (+1 producer warp)
+#endif
+constexpr int kWarps2D2 = STB200_2D2_NW;
+__host__ __device__ constexpr int k2d2_threads() { return (kWarps2D2 + 1) * 32; }
 #ifndef STB200_2D2_FBSEL
 #define STB200_2D2_FBSEL 1        // SHUFFLE fallback as one load + selects (0: predicated asm loads)
 #endif
 
 template <typename T, int NSW = 2> constexpr int k2d2_txo() { return (32 - 2 * (NSW - 1)) * vlen<T>(); }
 template <typename T, int NSW = 2>
-constexpr int k2d2_row_elems() { return kWarps2D * k2d2_txo<T, NSW>() + 2 * NSW * vlen<T>(); }
+constexpr int k2d2_row_elems() { return kWarps2D2 * k2d2_txo<T, NSW>() + 2 * NSW * vlen<T>(); }
 template <typename T, int NSW = 2>
 constexpr size_t k2d2_smem_bytes() {
-    return (size_t)kStages2D * (k2d2_row_elems<T, NSW>() * sizeof(T) + 2 * sizeof(uint64_t)) +
-           (size_t)(NSW - 1) * kWarps2D * (32 + 2) * vlen<T>() * sizeof(T);   // PLAIN: per-warp, per-level sweep row
+    return (size_t)kStages2D2 * (k2d2_row_elems<T, NSW>() * sizeof(T) + 2 * sizeof(uint64_t)) +
+           (size_t)(NSW - 1) * kWarps2D2 * (32 + 2) * vlen<T>() * sizeof(T);   // PLAIN: per-warp, per-level sweep row
 }
 
-// Grid: x = ceil(nx / (kWarps2D * TXO)), y = strips of H output rows
+// Minimum resident CTAs per SM (the register cap of __launch_bounds__).  Four
+// CTAs (20 warps, <= 96 registers) where the kernel fits without spilling,
+// else as many as its registers allow (measured on B200, 10 steps, Gpt/s
+// SHUFFLE / PLAIN): jacobi2d5 fp32 32768^2 three sweeps
+// 1908 / 1627 -> 2019 / 1631 at four, fp64 16384^2 914 / 789 -> 959 / 797,
+// jacobi2d9 fp32 1508 / 1537 -> 1611 / 1533; gaussblur separable fp32 8192^2 two
+// sweeps 1215 / 1214 -> 1088 (SHUFFLE spills at 96) / 1260.  -DSTB200_2D2_MINB
+// overrides every instance (A/B builds).
+template <class Op, typename T, int VAR, int NSW>
+constexpr int k2d2_minb() {
+#ifdef STB200_2D2_MINB
+    return STB200_2D2_MINB;
+#else
+    if (std::is_same<Op, OpJacobi2D5<T>>::value || std::is_same<Op, OpJacobi2D9<T>>::value) return 4;
+    if (IsSep<Op>::value && sizeof(T) == 4) return VAR == VAR_PLAIN && NSW == 2 ? 4 : 1;
+    return 1;
+#endif
+}
+
+// Grid: x = ceil(nx / (kWarps2D2 * TXO)), y = strips of H output rows
 // covering [y_lo, y_hi) (R <= y_lo, y_hi <= ny - R).  NSW sweeps per launch.
 template <class Op, typename T, int VARIANT, int NSW = 2>
-__global__ void __launch_bounds__(k2d_threads(), STB200_2D2_MINB)
+__global__ void __launch_bounds__(k2d2_threads(), (k2d2_minb<Op, T, VARIANT, NSW>()))
 k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo, int y_hi, int H,
      Coeffs<T, Op::NC> c) {
     static_assert(NSW == 2 || NSW == 3, "two or three sweeps per launch");
@@ -62,7 +86,7 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
     constexpr int W = V + 2 * R;
     constexpr int NW = 2 * R + 1;
     constexpr int WS = k2d2_row_elems<T, NSW>();
-    constexpr int S = kStages2D;
+    constexpr int S = kStages2D2;
     static_assert(R <= V, "halo wider than the staging pad");
     constexpr unsigned LOG2S = S == 2 ? 1 : S == 4 ? 2 : S == 8 ? 3 : S == 16 ? 4 : 5;
 
@@ -70,18 +94,18 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
     T* ring = reinterpret_cast<T*>(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * WS * sizeof(T));
     uint64_t* empty = full + S;
-    T* s1row = reinterpret_cast<T*>(empty + S);            // PLAIN: [NSW-1][kWarps2D][32V + 2V]
+    T* s1row = reinterpret_cast<T*>(empty + S);            // PLAIN: [NSW-1][kWarps2D2][32V + 2V]
 
     const int warp = threadIdx.x >> 5;
     const int lane = lane_id();
-    const int64_t X0 = (int64_t)blockIdx.x * (kWarps2D * TXO);       // CTA's first output column
+    const int64_t X0 = (int64_t)blockIdx.x * (kWarps2D2 * TXO);       // CTA's first output column
     const int ys = y_lo + (int)blockIdx.y * H;
     const int ye = min(ys + H, y_hi);
     if (ys >= ye) return;                                  // CTA-uniform
     const int row0 = ys - NSW * R;                         // first input row of the strip
     const int nrows = ye - ys + 2 * NSW * R;               // input rows [ys-NSW*R, ye+NSW*R)
     const int64_t n_left = (nx - X0 + TXO - 1) / TXO;
-    const int active = n_left < kWarps2D ? (int)n_left : kWarps2D;
+    const int active = n_left < kWarps2D2 ? (int)n_left : kWarps2D2;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -92,11 +116,11 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
     }
     __syncthreads();
 
-    if (warp == kWarps2D) {                                // ---- producer warp
+    if (warp == kWarps2D2) {                                // ---- producer warp
         if (lane == 0) {
             // staged element e <-> global column X0 - NSW*V + e; clip to [0, nx)
             const int64_t g_lo = X0 - NSW * V > 0 ? X0 - NSW * V : 0;
-            const int64_t g_hi0 = X0 + kWarps2D * TXO + NSW * V;
+            const int64_t g_hi0 = X0 + kWarps2D2 * TXO + NSW * V;
             const int64_t g_hi = g_hi0 < nx ? g_hi0 : nx;
             const uint32_t bytes = (uint32_t)((g_hi - g_lo) * (int64_t)sizeof(T));
             T* dst0 = ring + (g_lo - (X0 - NSW * V));
@@ -127,27 +151,25 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
 #pragma unroll
     for (int t = 0; t < Op::NC; ++t) cr.c[t] = c.c[t];
     // separable kinds (OpGauss5Sep): a window row keeps the row-pass values
-    // in its centre slots and the raw centre values in its halo slots
-    // (needed for the held boundary ring); slot of raw element p:
-    auto raw_slot = [](int p) { return p < R ? p : V + p; };
+    // in its centre slots.  The held value of a boundary-ring cell (EDGE
+    // path, below) is the raw input value, re-read from the row ring: the
+    // ring keeps HOLD more rows resident for it.  (Keeping the raw values in
+    // the window held ~27 more registers live in the whole kernel; re-reading
+    // them from global memory stalled the edge warps on every row: -17%.)
+    constexpr unsigned HOLD = IsSep<Op>::value ? (NSW - 1) * R : 0;
+    static_assert(STB200_REL_LAG || HOLD == 0, "held rows need the lagged release");
     auto sep_row = [&](T* d) {
         if constexpr (IsSep<Op>::value) {
-            static_assert(V <= 2 * R, "raw centre values must fit the halo slots");
-            T hv[V], rv[V];
-#pragma unroll
-            for (int k = 0; k < V; ++k) rv[k] = d[R + k];
+            T hv[V];
             Op::template rowpass<V>(d, hv, cr);
 #pragma unroll
-            for (int k = 0; k < V; ++k) {
-                d[R + k] = hv[k];
-                d[raw_slot(k)] = rv[k];
-            }
+            for (int k = 0; k < V; ++k) d[R + k] = hv[k];
         }
     };
     const uint32_t rt_zero = (uint32_t)((uint64_t)nx >> 48);   // 0 at run time, unknown to the compiler
     auto consume = [&](unsigned r, T* dst) {
         const unsigned s = r & (S - 1);
-        if (STB200_REL_LAG) ring_release_lagged<S, VARIANT == VAR_PLAIN ? 4 : 1>(empty, r);   // rows before r (pipe.cuh)
+        if (STB200_REL_LAG) ring_release_lagged<S, VARIANT == VAR_PLAIN ? 4 : 1, HOLD>(empty, r);   // rows before r - HOLD (pipe.cuh)
         mbar_wait(&full[s], (r >> LOG2S) & 1u);
         const T* row = ring + s * WS;
         T v[V];
@@ -210,7 +232,7 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
     // One row per level: with a single row shared by the levels, the
     // three-sweep PLAIN kernel gave run-to-run differences (tools/flake_hunt.py,
     // jacobi2d5 32768^2: 7 of 8 repeats) although __syncwarp orders each reuse.
-    auto srow_of = [&](int k) { return s1row + ((k - 1) * kWarps2D + warp) * (32 + 2) * V + V; };
+    auto srow_of = [&](int k) { return s1row + ((k - 1) * kWarps2D2 + warp) * (32 + 2) * V + V; };
 
     auto point_row = [&](const auto& w, T* o) {
         if constexpr (IsSep<Op>::value && HasPaired<Op>::value) {
@@ -282,9 +304,9 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
                     const bool yint = yk >= R && yk < ny - R;
 #pragma unroll
                     for (int p = 0; p < V; ++p) {               // boundary ring: held value
-                        const T held = IsSep<Op>::value ? wl[k - 1][(ph + R) % NW][raw_slot(p)]
-                                                        : wl[k - 1][(ph + R) % NW][R + p];
-                        if (!(yint && xin[p])) v[p] = held;
+                        if (!(yint && xin[p]))
+                            v[p] = IsSep<Op>::value ? ring[((unsigned)(yk - row0) & (S - 1)) * WS + lo_e + p]
+                                                    : wl[k - 1][(ph + R) % NW][R + p];
                     }
                 }
                 halo(v, wl[k][u % NW], k);
@@ -322,8 +344,12 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
     const bool stores_lane = lane >= NSW - 1 && lane <= 32 - NSW;
     const bool rows_inner = ys - (NSW - 1) * R >= R && ye + (NSW - 1) * R <= ny - R;
     const bool interior = __all_sync(FULL, all_x && (vec_store || !stores_lane)) && rows_inner;
+#ifdef STB200_2D2_NOEDGE
+    march(std::false_type{});                              // experiment: register count of the interior path
+#else
     if (interior) march(std::false_type{});
     else march(std::true_type{});
+#endif
 }
 
 }  // namespace stb200

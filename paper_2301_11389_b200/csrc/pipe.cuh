@@ -70,9 +70,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 #ifndef STB200_REL_BATCH
 #define STB200_REL_BATCH 0
 #endif
-template <unsigned S, unsigned B0 = 1>
-__device__ __forceinline__ void ring_release_lagged(uint64_t* empty, unsigned r) {
+// D > 0 keeps D more rows resident (released D rows later): k2d2 re-reads
+// the raw input row of a window centre for the held boundary-ring values.
+template <unsigned S, unsigned B0 = 1, unsigned D = 0>
+__device__ __forceinline__ void ring_release_lagged(uint64_t* empty, unsigned r_) {
     constexpr unsigned B = STB200_REL_BATCH > 0 ? STB200_REL_BATCH : B0;
+    static_assert(D + B < S, "the producer needs a free stage");
+    if (r_ < D) return;
+    const unsigned r = r_ - D;
     if (r == 0 || r % B != 0) return;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #pragma unroll

@@ -99,6 +99,20 @@ def test_graph_cache_and_variant_switch(oracle):
         assert np.array_equal(r.view(np.uint8), results[0].view(np.uint8))
 
 
+@pytest.mark.parametrize("kind,dtype,expect", [
+    ("gaussblur5x5", "f32", "plain"), ("jacobi2d5", "f32", "shuffle"), ("tricubic", "f32", "plain"),
+    ("lapgsrb", "f32", "shuffle"), ("gameoflife", "i32", "plain")])
+def test_auto_variant_resolves_per_kind(kind, dtype, expect):
+    """ST_AUTO resolves in the library to the kind's measured-faster variant
+    (stencil.h) and stencil_get_variant reports it."""
+    shape = (12, 12, 132) if kind in ("tricubic", "lapgsrb") else (40, 136)
+    st = Stencil(kind, shape[::-1], dtype, variant="auto")
+    assert st.variant == expect
+    assert st.info()["variant"] == (0 if expect == "shuffle" else 1)
+    st.set_variant("shuffle")
+    assert st.variant == "shuffle"
+
+
 def test_run_on_a_side_stream_and_zero_iterations():
     shape = (20, 132)
     f = inputs.generate_np(shape, "f32", 6)

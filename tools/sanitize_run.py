@@ -9,6 +9,16 @@ paths (ktb2r, ktb2d, k2d2 two / three sweeps) and the paper-literal family.
 
 Every output is also checked against the CPU oracle (tests/parity.py), so a
 run under a tool that perturbs timing still proves the results.
+
+Guard bands (always on; the gpurun pool refuses compute-sanitizer, so this is
+the bounds check that runs there): every device buffer is a 16-byte-aligned
+slice in the middle of a larger allocation whose GUARD elements before and
+after are poisoned (NaN for floating point, 0x7f7f7f7f for int32).  A kernel
+that writes outside its buffer changes a guard (checked bit for bit after
+every run); one that reads outside its buffer into a result turns that
+result NaN / garbage (caught by the oracle comparison).
+
+    python tools/sanitize_run.py           # no tool: guard bands + oracle parity
 """
 import argparse
 import os
@@ -29,18 +39,9 @@ from parity import assert_parity  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--quick", action="store_true", help="one shape per kind, SHUFFLE + PLAIN only")
 ap.add_argument("--canary", action="store_true",
-                help="a deliberately undersized output buffer: memcheck MUST report errors "
-                     "(proves the tool instruments this library's kernels)")
+                help="a deliberately undersized output buffer: the guard check MUST fire "
+                     "(proves the guards see this library's out-of-bounds writes)")
 a = ap.parse_args()
-
-if a.canary:
-    st = Stencil("jacobi2d5", (260, 37), "f32")
-    src = torch.ones((37, 260), device="cuda")
-    dst = torch.zeros((4, 260), device="cuda")      # 33 rows short: the kernel writes past it
-    st.step([src], [dst])
-    torch.cuda.synchronize()
-    print("canary launched")
-    sys.exit(0)
 
 KINDS2 = ["jacobi2d5", "jacobi2d9", "gaussblur5x5", "gameoflife", "whispering"]
 KINDS3 = ["laplacian3d7", "jacobi3d7", "wave13pt", "divergence", "gradient", "tricubic", "tricubic2",
@@ -49,6 +50,49 @@ SH2 = [(37, 260), (9, 132)] if not a.quick else [(37, 260)]
 SH3 = [(9, 35, 132), (6, 7, 68)] if not a.quick else [(9, 35, 132)]
 PAPER = ["paper_original", "paper_ptxasw", "paper_noload", "paper_nocorner", "paper_uniform"]
 n_checked = 0
+GUARD = 4096                      # elements on each side (16 / 32 KiB)
+POISON = {"f32": float("nan"), "f64": float("nan"), "i32": 0x7f7f7f7f}
+
+
+def guarded(host: np.ndarray):
+    """Device copy of `host` inside a poisoned allocation: (view, whole)."""
+    n = host.size
+    whole = torch.empty(n + 2 * GUARD, dtype=torch.from_numpy(host[:0].reshape(-1)).dtype, device="cuda")
+    whole.fill_(POISON["i32" if host.dtype == np.int32 else "f32"])
+    view = whole[GUARD:GUARD + n].view(host.shape)
+    view.copy_(torch.from_numpy(host))
+    assert view.data_ptr() % 16 == 0
+    return view, whole
+
+
+def check_guards(wholes, what):
+    for w in wholes:
+        h = w.cpu().numpy()
+        for part in (h[:GUARD], h[-GUARD:]):
+            if part.dtype == np.int32:
+                ok = np.all(part == 0x7f7f7f7f)
+            else:
+                ok = np.all(np.isnan(part)) and np.all(part.view(np.uint32 if part.dtype == np.float32
+                                                                    else np.uint64) == part[:1].view(
+                    np.uint32 if part.dtype == np.float32 else np.uint64))
+            assert ok, f"{what}: a guard band was overwritten (out-of-bounds write)"
+
+
+if a.canary:
+    # a deliberately undersized output buffer: the guard check MUST fire
+    # (proves the guards see this library's out-of-bounds writes)
+    st = Stencil("jacobi2d5", (260, 37), "f32")
+    src, _ = guarded(np.ones((37, 260), np.float32))
+    dst, whole = guarded(np.zeros((30, 260), np.float32))  # 7 rows short: writes land in the guard
+    st.step([src], [dst])
+    torch.cuda.synchronize()
+    try:
+        check_guards([whole], "canary")
+    except AssertionError as e:
+        print("canary detected:", e)
+        sys.exit(0)
+    print("canary NOT detected")
+    sys.exit(1)
 
 
 def dtypes(kind):
@@ -77,9 +121,11 @@ def check_run(kind, dtype, shape, variant, n, fusion=None):
     st = Stencil(kind, shape[::-1], dtype, variant=variant)
     if fusion is not None:
         st.set_fusion(fusion)
-    d = [torch.from_numpy(b.copy()).cuda() for b in bufs]
+    gb = [guarded(b) for b in bufs]
+    d = [v for v, _ in gb]
     gidx = st.run(d, n)
     torch.cuda.synchronize()
+    check_guards([w for _, w in gb], f"{kind} {dtype} {shape} {variant} n={n} fusion={fusion}")
     nres = 1 if ar["n_bufs"] == 2 or (ar["n_bufs"] == 3 and ar["n_in"] == 2) else ar["n_out"]
     lo, hi = ar["lo"], ar["hi"]
     sl = tuple(slice(lo, m - hi) for m in shape)
@@ -120,9 +166,10 @@ for kind in ("jacobi2d5", "gameoflife", "laplacian3d7", "wave13pt", "gradient", 
             # ablations are invalid at warp edges by design: launch only
             st = Stencil(kind, shape[::-1], dt, variant=var)
             ar, bufs = bufs_of(kind, dt, shape, 5)
-            d = [torch.from_numpy(b.copy()).cuda() for b in bufs]
-            st.run(d, 1)
+            gb = [guarded(b) for b in bufs]
+            st.run([v for v, _ in gb], 1)
             torch.cuda.synchronize()
+            check_guards([w for _, w in gb], f"{kind} {var}")
             st.close()
         else:
             check_run(kind, dt, shape, var, 2)

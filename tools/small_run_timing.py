@@ -15,11 +15,21 @@ from paper_2301_11389_b200 import inputs  # noqa: E402
 from paper_2301_11389_b200.binding import Stencil  # noqa: E402
 
 
-def timed(fn, flush, reps=30):
+rd = torch.empty(64 << 20, device="cuda")
+
+
+def timed(fn, flush, reps=30, queued=False, read=False):
+    """median / min microseconds between events around fn(); queued=True
+    keeps the GPU busy (a 50 us spin kernel after the flush) while the host
+    submits, so host-side call overhead cannot open a gap in the window."""
     ts = []
     for _ in range(reps):
         if flush is not None:
             flush.fill_(1.0)
+        if read:
+            rd.sum()                  # a read of another > L2 buffer: evicts the flush's dirty lines
+        if queued:
+            torch.cuda._sleep(100000)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -42,6 +52,14 @@ for fl in (None, flush):
     print("empty-kernel graph", "flush" if fl is not None else "warm", "median/min us", timed(g.replay, fl))
     print("empty-kernel direct launch", "flush" if fl is not None else "warm", "median/min us",
           timed(lambda: x.add_(1.0), fl))
+print("empty-kernel direct launch flush+queued median/min us", timed(lambda: x.add_(1.0), flush, queued=True))
+print("empty-kernel graph flush+queued median/min us", timed(g.replay, flush, queued=True))
+print("empty-kernel direct launch warm+queued median/min us", timed(lambda: x.add_(1.0), None, queued=True))
+print("no kernel at all (two events) flush+queued median/min us", timed(lambda: None, flush, queued=True))
+print("no kernel at all (two events) warm+queued median/min us", timed(lambda: None, None, queued=True))
+print("empty-kernel direct launch flush+read median/min us", timed(lambda: x.add_(1.0), flush, read=True))
+print("empty-kernel direct launch flush+read+queued median/min us",
+      timed(lambda: x.add_(1.0), flush, read=True, queued=True))
 for variant in ("shuffle", "plain"):
     for n in (0, 1, 10):
         st = Stencil("jacobi2d5", (512, 512), "f32", variant=variant)
@@ -53,4 +71,10 @@ for variant in ("shuffle", "plain"):
         for fl in (None, flush):
             print(variant, "n_iters", n, "flush" if fl is not None else "warm", "median/min us",
                   timed(lambda: st.run([a, b], n), fl))
+        print(variant, "n_iters", n, "flush+queued", "median/min us",
+              timed(lambda: st.run([a, b], n), flush, queued=True))
+        print(variant, "n_iters", n, "warm+queued", "median/min us",
+              timed(lambda: st.run([a, b], n), None, queued=True))
+        print(variant, "n_iters", n, "flush+read", "median/min us",
+              timed(lambda: st.run([a, b], n), flush, read=True))
         st.close()
