@@ -175,12 +175,13 @@ static cudaError_t launch_k2d2(const stencil_s* h, const void* in, void* out, cu
     // 1459 (128) Gpt/s, flat to 512; fp64 16384^2 best at 48-64
     constexpr int kStripH = sizeof(T) == 8 ? 64 : 128;
     auto kern = k2d2<Op, T, VAR, NSW>;
-    constexpr size_t smem = k2d2_smem_bytes<T, NSW>();
-    kernel_setup((const void*)kern, h->device, smem, k2d2_threads());
+    constexpr int NW = k2d2_nw<Op, T, VAR, NSW>();
+    constexpr size_t smem = k2d2_smem_bytes<T, NSW, NW>();
+    kernel_setup((const void*)kern, h->device, smem, k2d2_threads<NW>());
     const int64_t nx = h->ldims[0], ny = h->ldims[1];
     const int64_t y_lo = R, y_hi = ny - R;
     if (y_hi <= y_lo) return cudaSuccess;
-    const int64_t gx = (nx + kWarps2D2 * k2d2_txo<T, NSW>() - 1) / (kWarps2D2 * k2d2_txo<T, NSW>());
+    const int64_t gx = (nx + NW * k2d2_txo<T, NSW>() - 1) / (NW * k2d2_txo<T, NSW>());
     const int64_t rows = y_hi - y_lo;
     static const int dbg_h = getenv("STB200_2D2_H") ? atoi(getenv("STB200_2D2_H")) : 0;
     int64_t H = (rows * gx + 2 * sm_count(h->device) - 1) / (2 * sm_count(h->device));
@@ -190,7 +191,7 @@ static cudaError_t launch_k2d2(const stencil_s* h, const void* in, void* out, cu
     if (nstrips > 65535 || ny > INT32_MAX) return cudaErrorInvalidConfiguration;
     Coeffs<T, Op::NC> c{};
     for (int t = 0; t < Op::NC; ++t) c.c[t] = (T)op_coeff<Op>(h, t);
-    kern<<<dim3((unsigned)gx, (unsigned)nstrips), k2d2_threads(), smem, s>>>(
+    kern<<<dim3((unsigned)gx, (unsigned)nstrips), k2d2_threads<NW>(), smem, s>>>(
         (const T*)in, (T*)out, nx, (int)ny, (int)y_lo, (int)y_hi, (int)H, c);
     return cudaGetLastError();
 }
@@ -228,12 +229,12 @@ template <int VAR, int NSW>
 static cudaError_t launch_life(const stencil_s* h, const void* in, void* out, cudaStream_t s) {
     constexpr int kStripH = 128;
     auto kern = k2dlife<VAR, NSW>;
-    constexpr size_t smem = k2d2_smem_bytes<int, NSW>();
-    kernel_setup((const void*)kern, h->device, smem, k2d2_threads());
+    constexpr size_t smem = k2d2_smem_bytes<int, NSW, kWarpsLife>();
+    kernel_setup((const void*)kern, h->device, smem, k2d2_threads<kWarpsLife>());
     const int64_t nx = h->ldims[0], ny = h->ldims[1];
     const int64_t y_lo = 1, y_hi = ny - 1;
     if (y_hi <= y_lo) return cudaSuccess;
-    const int64_t gx = (nx + kWarps2D2 * k2d2_txo<int, NSW>() - 1) / (kWarps2D2 * k2d2_txo<int, NSW>());
+    const int64_t gx = (nx + kWarpsLife * k2d2_txo<int, NSW>() - 1) / (kWarpsLife * k2d2_txo<int, NSW>());
     const int64_t rows = y_hi - y_lo;
     static const int dbg_h = getenv("STB200_2D2_H") ? atoi(getenv("STB200_2D2_H")) : 0;
     int64_t H = (rows * gx + 2 * sm_count(h->device) - 1) / (2 * sm_count(h->device));
@@ -241,7 +242,7 @@ static cudaError_t launch_life(const stencil_s* h, const void* in, void* out, cu
     if (dbg_h > 0) H = dbg_h;
     const int64_t nstrips = (rows + H - 1) / H;
     if (nstrips > 65535 || ny > INT32_MAX) return cudaErrorInvalidConfiguration;
-    kern<<<dim3((unsigned)gx, (unsigned)nstrips), k2d2_threads(), smem, s>>>(
+    kern<<<dim3((unsigned)gx, (unsigned)nstrips), k2d2_threads<kWarpsLife>(), smem, s>>>(
         (const int*)in, (int*)out, nx, (int)ny, (int)y_lo, (int)y_hi, (int)H);
     return cudaGetLastError();
 }

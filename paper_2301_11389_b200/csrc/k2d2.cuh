@@ -36,56 +36,65 @@ namespace stb200 {
 #define STB200_2D2_S 16           // staged rows per CTA (ring stages); power of 2
 #endif
 constexpr int kStages2D2 = STB200_2D2_S;
-#ifndef STB200_2D2_NW
-#define STB200_2D2_NW 4           // consumer warps per CTA (+1 producer warp)
-#endif
-constexpr int kWarps2D2 = STB200_2D2_NW;
-__host__ __device__ constexpr int k2d2_threads() { return (kWarps2D2 + 1) * 32; }
+template <int NW> __host__ __device__ constexpr int k2d2_threads() { return (NW + 1) * 32; }
 #ifndef STB200_2D2_FBSEL
 #define STB200_2D2_FBSEL 1        // SHUFFLE fallback as one load + selects (0: predicated asm loads)
 #endif
 
 template <typename T, int NSW = 2> constexpr int k2d2_txo() { return (32 - 2 * (NSW - 1)) * vlen<T>(); }
-template <typename T, int NSW = 2>
-constexpr int k2d2_row_elems() { return kWarps2D2 * k2d2_txo<T, NSW>() + 2 * NSW * vlen<T>(); }
-template <typename T, int NSW = 2>
+template <typename T, int NSW, int NW>
+constexpr int k2d2_row_elems() { return NW * k2d2_txo<T, NSW>() + 2 * NSW * vlen<T>(); }
+template <typename T, int NSW, int NW>
 constexpr size_t k2d2_smem_bytes() {
-    return (size_t)kStages2D2 * (k2d2_row_elems<T, NSW>() * sizeof(T) + 2 * sizeof(uint64_t)) +
-           (size_t)(NSW - 1) * kWarps2D2 * (32 + 2) * vlen<T>() * sizeof(T);   // PLAIN: per-warp, per-level sweep row
+    return (size_t)kStages2D2 * (k2d2_row_elems<T, NSW, NW>() * sizeof(T) + 2 * sizeof(uint64_t)) +
+           (size_t)(NSW - 1) * NW * (32 + 2) * vlen<T>() * sizeof(T);   // PLAIN: per-warp, per-level sweep row
 }
 
-// Minimum resident CTAs per SM (the register cap of __launch_bounds__).  Four
-// CTAs (20 warps, <= 96 registers) where the kernel fits without spilling,
-// else as many as its registers allow (measured on B200, 10 steps, Gpt/s
-// SHUFFLE / PLAIN): jacobi2d5 fp32 32768^2 three sweeps
-// 1908 / 1627 -> 2019 / 1631 at four, fp64 16384^2 914 / 789 -> 959 / 797,
-// jacobi2d9 fp32 1508 / 1537 -> 1611 / 1533; gaussblur separable fp32 8192^2 two
-// sweeps 1215 / 1214 -> 1088 (SHUFFLE spills at 96) / 1260.  -DSTB200_2D2_MINB
-// overrides every instance (A/B builds).
+// Consumer warps per CTA (+1 producer warp) and minimum resident CTAs per
+// SM (the register cap of __launch_bounds__), per instance.  Eight consumer
+// warps and two CTAs (18 warps, <= 96 registers) where the kernel fits: the
+// producer warp's registers are shared by twice the consumers.  Measured on
+// B200 (10 steps, Gpt/s SHUFFLE / PLAIN, profiles/r02_ab_minb.txt,
+// r02_ab_nw8.txt), against 4 consumer warps at 3 CTAs (the registers' limit):
+//   jacobi2d5 fp32 32768^2 three sweeps 1908 / 1627 -> 2019 / 1669,
+//   jacobi2d5 fp64 16384^2 three sweeps 914 / 789 -> 987 / 813,
+//   jacobi2d9 fp32 two sweeps 1508 / 1537 -> 1610 / 1547 (4 x 4 warps),
+//   gaussblur separable fp32 8192^2 two sweeps 1205 / 1353 -> 1361 / 1390.
+// The others keep 4 consumer warps and as many CTAs as their registers
+// allow.  -DSTB200_2D2_NW / -DSTB200_2D2_MINB override every instance (A/Bs).
+template <class Op, typename T, int VAR, int NSW>
+constexpr int k2d2_nw() {
+#ifdef STB200_2D2_NW
+    return STB200_2D2_NW;
+#else
+    if (std::is_same<Op, OpJacobi2D5<T>>::value || std::is_same<Op, OpJacobi2D9<T>>::value) return 8;
+    if (IsSep<Op>::value && sizeof(T) == 4 && NSW == 2) return 8;
+    return 4;
+#endif
+}
 template <class Op, typename T, int VAR, int NSW>
 constexpr int k2d2_minb() {
 #ifdef STB200_2D2_MINB
     return STB200_2D2_MINB;
 #else
-    if (std::is_same<Op, OpJacobi2D5<T>>::value || std::is_same<Op, OpJacobi2D9<T>>::value) return 4;
-    if (IsSep<Op>::value && sizeof(T) == 4) return VAR == VAR_PLAIN && NSW == 2 ? 4 : 1;
-    return 1;
+    return k2d2_nw<Op, T, VAR, NSW>() == 8 ? 2 : 1;
 #endif
 }
 
-// Grid: x = ceil(nx / (kWarps2D2 * TXO)), y = strips of H output rows
+// Grid: x = ceil(nx / (NW * TXO)), y = strips of H output rows
 // covering [y_lo, y_hi) (R <= y_lo, y_hi <= ny - R).  NSW sweeps per launch.
 template <class Op, typename T, int VARIANT, int NSW = 2>
-__global__ void __launch_bounds__(k2d2_threads(), (k2d2_minb<Op, T, VARIANT, NSW>()))
+__global__ void __launch_bounds__(k2d2_threads<k2d2_nw<Op, T, VARIANT, NSW>()>(), (k2d2_minb<Op, T, VARIANT, NSW>()))
 k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo, int y_hi, int H,
      Coeffs<T, Op::NC> c) {
     static_assert(NSW == 2 || NSW == 3, "two or three sweeps per launch");
     constexpr int R = Op::R;
     constexpr int V = vlen<T>();
     constexpr int TXO = k2d2_txo<T, NSW>();
+    constexpr int kWarps2D2 = k2d2_nw<Op, T, VARIANT, NSW>();
     constexpr int W = V + 2 * R;
     constexpr int NW = 2 * R + 1;
-    constexpr int WS = k2d2_row_elems<T, NSW>();
+    constexpr int WS = k2d2_row_elems<T, NSW, kWarps2D2>();
     constexpr int S = kStages2D2;
     static_assert(R <= V, "halo wider than the staging pad");
     constexpr unsigned LOG2S = S == 2 ? 1 : S == 4 ? 2 : S == 8 ? 3 : S == 16 ? 4 : 5;

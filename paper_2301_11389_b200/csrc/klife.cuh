@@ -35,6 +35,8 @@
 
 namespace stb200 {
 
+constexpr int kWarpsLife = 4;   // consumer warps per CTA (+1 producer); 8 measured even (r02_ab_nw8.txt)
+
 __device__ __forceinline__ uint32_t life_pack(const int* v) {
     const uint32_t a = __byte_perm((uint32_t)v[0], (uint32_t)v[1], 0x0040);
     const uint32_t b = __byte_perm((uint32_t)v[2], (uint32_t)v[3], 0x0040);
@@ -53,12 +55,12 @@ __device__ __forceinline__ uint32_t life_rule(uint32_t n9, uint32_t p) {
 }
 
 template <int VARIANT, int NSW = 2>
-__global__ void __launch_bounds__(k2d2_threads())
+__global__ void __launch_bounds__(k2d2_threads<kWarpsLife>())
 k2dlife(const int* __restrict__ in, int* __restrict__ out, int64_t nx, int ny, int y_lo, int y_hi, int H) {
     static_assert(NSW == 2 || NSW == 3, "two or three sweeps per launch");
     constexpr int R = 1, V = 4, NW = 3;
     constexpr int TXO = k2d2_txo<int, NSW>();
-    constexpr int WS = k2d2_row_elems<int, NSW>();
+    constexpr int WS = k2d2_row_elems<int, NSW, kWarpsLife>();
     constexpr int S = kStages2D2;
     constexpr unsigned LOG2S = S == 2 ? 1 : S == 4 ? 2 : S == 8 ? 3 : S == 16 ? 4 : 5;
 
@@ -66,18 +68,18 @@ k2dlife(const int* __restrict__ in, int* __restrict__ out, int64_t nx, int ny, i
     int* ring = reinterpret_cast<int*>(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * WS * sizeof(int));
     uint64_t* empty = full + S;
-    uint32_t* s1row = reinterpret_cast<uint32_t*>(empty + S);   // PLAIN: [kWarps2D2][34] words
+    uint32_t* s1row = reinterpret_cast<uint32_t*>(empty + S);   // PLAIN: [kWarpsLife][34] words
 
     const int warp = threadIdx.x >> 5;
     const int lane = lane_id();
-    const int64_t X0 = (int64_t)blockIdx.x * (kWarps2D2 * TXO);
+    const int64_t X0 = (int64_t)blockIdx.x * (kWarpsLife * TXO);
     const int ys = y_lo + (int)blockIdx.y * H;
     const int ye = min(ys + H, y_hi);
     if (ys >= ye) return;
     const int row0 = ys - NSW * R;
     const int nrows = ye - ys + 2 * NSW * R;
     const int64_t n_left = (nx - X0 + TXO - 1) / TXO;
-    const int active = n_left < kWarps2D2 ? (int)n_left : kWarps2D2;
+    const int active = n_left < kWarpsLife ? (int)n_left : kWarpsLife;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -88,10 +90,10 @@ k2dlife(const int* __restrict__ in, int* __restrict__ out, int64_t nx, int ny, i
     }
     __syncthreads();
 
-    if (warp == kWarps2D2) {                                // ---- producer warp (as k2d2)
+    if (warp == kWarpsLife) {                                // ---- producer warp (as k2d2)
         if (lane == 0) {
             const int64_t g_lo = X0 - NSW * V > 0 ? X0 - NSW * V : 0;
-            const int64_t g_hi0 = X0 + kWarps2D2 * TXO + NSW * V;
+            const int64_t g_hi0 = X0 + kWarpsLife * TXO + NSW * V;
             const int64_t g_hi = g_hi0 < nx ? g_hi0 : nx;
             const uint32_t bytes = (uint32_t)((g_hi - g_lo) * (int64_t)sizeof(int));
             int* dst0 = ring + (g_lo - (X0 - NSW * V));
