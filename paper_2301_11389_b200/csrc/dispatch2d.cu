@@ -176,7 +176,7 @@ static cudaError_t launch_k2d2(const stencil_s* h, const void* in, void* out, cu
     constexpr int kStripH = sizeof(T) == 8 ? 64 : 128;
     auto kern = k2d2<Op, T, VAR, NSW>;
     constexpr int NW = k2d2_nw<Op, T, VAR, NSW>();
-    constexpr size_t smem = k2d2_smem_bytes<T, NSW, NW>();
+    constexpr size_t smem = k2d2_smem_bytes<T, NSW, NW, k2d2_stages<R, T>()>();
     kernel_setup((const void*)kern, h->device, smem, k2d2_threads<NW>());
     const int64_t nx = h->ldims[0], ny = h->ldims[1];
     const int64_t y_lo = R, y_hi = ny - R;

@@ -36,6 +36,30 @@ namespace stb200 {
 #define STB200_2D2_S 16           // staged rows per CTA (ring stages); power of 2
 #endif
 constexpr int kStages2D2 = STB200_2D2_S;
+// STB200_2D2_CT = 1: the ring has a multiple of the window height NW = 2R+1
+// stages and the march is unrolled by the stage count, so a row's ring slot,
+// its mbarriers and the stage it releases are compile-time constants (only
+// the phase bit is carried); 0: power-of-two ring, slots computed per row.
+// Measured (profiles/r02_ab_ct.txt, Gpt/s SHUFFLE / PLAIN, power-of-two 16
+// stages -> compile-time slots): jacobi2d5 fp32 32768^2 2016 / 1665 -> 2043 /
+// 1687, jacobi2d9 1588 / 1536 -> 1636 / 1634, gaussblur 8192^2 x100 1363 /
+// 1384 -> 1380 / 1395 (10 stages, PLAIN releases in pairs; 20 stages: SHUFFLE
+// 1228, batches of 5: PLAIN 1260), fp64 jacobi2d5 even.
+#ifndef STB200_2D2_CT
+#define STB200_2D2_CT 1
+#endif
+#ifndef STB200_2D2_S2
+#define STB200_2D2_S2 10          // CT ring stages for radius 2 (a multiple of 5)
+#endif
+#ifndef STB200_2D2_RBP
+#define STB200_2D2_RBP 0          // CT: PLAIN release batch (0: 4 if it divides S, else 2)
+#endif
+// compile-time slots for the 32-bit kernels (the fp64 three-sweep kernels
+// would spill at their register cap: 136 / 116 bytes)
+template <int R, typename T> constexpr bool k2d2_ct() { return STB200_2D2_CT && sizeof(T) == 4; }
+template <int R, typename T> constexpr int k2d2_stages() {
+    return k2d2_ct<R, T>() ? (R == 1 ? 12 : STB200_2D2_S2) : kStages2D2;
+}
 template <int NW> __host__ __device__ constexpr int k2d2_threads() { return (NW + 1) * 32; }
 #ifndef STB200_2D2_FBSEL
 #define STB200_2D2_FBSEL 1        // SHUFFLE fallback as one load + selects (0: predicated asm loads)
@@ -44,9 +68,9 @@ template <int NW> __host__ __device__ constexpr int k2d2_threads() { return (NW 
 template <typename T, int NSW = 2> constexpr int k2d2_txo() { return (32 - 2 * (NSW - 1)) * vlen<T>(); }
 template <typename T, int NSW, int NW>
 constexpr int k2d2_row_elems() { return NW * k2d2_txo<T, NSW>() + 2 * NSW * vlen<T>(); }
-template <typename T, int NSW, int NW>
+template <typename T, int NSW, int NW, int S = kStages2D2>
 constexpr size_t k2d2_smem_bytes() {
-    return (size_t)kStages2D2 * (k2d2_row_elems<T, NSW, NW>() * sizeof(T) + 2 * sizeof(uint64_t)) +
+    return (size_t)S * (k2d2_row_elems<T, NSW, NW>() * sizeof(T) + 2 * sizeof(uint64_t)) +
            (size_t)(NSW - 1) * NW * (32 + 2) * vlen<T>() * sizeof(T);   // PLAIN: per-warp, per-level sweep row
 }
 
@@ -95,9 +119,11 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
     constexpr int W = V + 2 * R;
     constexpr int NW = 2 * R + 1;
     constexpr int WS = k2d2_row_elems<T, NSW, kWarps2D2>();
-    constexpr int S = kStages2D2;
+    constexpr int S = k2d2_stages<R, T>();
     static_assert(R <= V, "halo wider than the staging pad");
-    constexpr unsigned LOG2S = S == 2 ? 1 : S == 4 ? 2 : S == 8 ? 3 : S == 16 ? 4 : 5;
+    constexpr bool CT = k2d2_ct<R, T>();
+    static_assert(!CT || S % NW == 0, "compile-time slots: S a multiple of the window height");
+    static_assert(CT || (S & (S - 1)) == 0, "power-of-two ring");
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* ring = reinterpret_cast<T*>(smem_raw);
@@ -133,9 +159,9 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
             const int64_t g_hi = g_hi0 < nx ? g_hi0 : nx;
             const uint32_t bytes = (uint32_t)((g_hi - g_lo) * (int64_t)sizeof(T));
             T* dst0 = ring + (g_lo - (X0 - NSW * V));
-            for (int r = 0; r < nrows; ++r) {
-                const unsigned s = (unsigned)r & (S - 1);
-                if (r >= S) mbar_wait_backoff<512>(&empty[s], (((unsigned)r >> LOG2S) - 1) & 1u);
+            unsigned s = 0, ph = 0;                        // slot of row r, phase of its (r / S)-th use
+            for (int r = 0; r < nrows; ++r, s = s + 1 == S ? (ph ^= 1u, 0u) : s + 1) {
+                if (r >= S) mbar_wait_backoff<512>(&empty[s], ph ^ 1u);
                 const int yin = row0 + r;
                 if (yin >= 0 && yin < ny) {
                     mbar_arrive_expect_tx(&full[s], bytes);
@@ -176,10 +202,27 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
         }
     };
     const uint32_t rt_zero = (uint32_t)((uint64_t)nx >> 48);   // 0 at run time, unknown to the compiler
-    auto consume = [&](unsigned r, T* dst) {
-        const unsigned s = r & (S - 1);
-        if (STB200_REL_LAG) ring_release_lagged<S, VARIANT == VAR_PLAIN ? 4 : 1, HOLD>(empty, r);   // rows before r - HOLD (pipe.cuh)
-        mbar_wait(&full[s], (r >> LOG2S) & 1u);
+    // rows released per fence (pipe.cuh ring_release_lagged): 4 for PLAIN,
+    // 1 for SHUFFLE; with compile-time slots a divisor of S
+    constexpr unsigned RB = VARIANT == VAR_PLAIN ? (STB200_2D2_RBP ? STB200_2D2_RBP : S % 4 == 0 ? 4 : 2) : 1;
+    static_assert(!CT || S % RB == 0, "release batch divides the ring");
+    // consume input row r from ring slot s (= r mod S) whose fill phase is par
+    auto consume = [&](unsigned r, unsigned s, unsigned par, T* dst) {
+        if constexpr (CT) {
+            // release rows r-HOLD-RB .. r-HOLD-1 when (r - HOLD) % RB == 0:
+            // slots and condition are compile-time (s is), one runtime guard
+            if (STB200_REL_LAG && (s + S - HOLD % S) % RB == 0 && r >= HOLD + RB) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+                for (unsigned k = 0; k < RB; ++k)
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                                     smem_u32(&empty[(s + 2 * S - HOLD - RB + k) % S]))
+                                 : "memory");
+            }
+        } else if (STB200_REL_LAG) {
+            ring_release_lagged<S, RB, HOLD>(empty, r);   // rows before r - HOLD (pipe.cuh)
+        }
+        mbar_wait(&full[s], par);
         const T* row = ring + s * WS;
         T v[V];
         {
@@ -288,6 +331,8 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
         }
     };
 
+    const int nt = ye - ys + 2 * (NSW - 1) * R;            // sweep-1 rows
+    unsigned par_it = 0;                                   // CT: phase of ring pass t / S
     // one staged input row at step t (phase u = t mod NW, compile time after
     // unrolling).  Sweep-1 row y1 = ys - (NSW-1)R + t; sweep-k row
     // y1 - (k-1)R exists once t >= 2R(k-1).  EDGE = false: the warp's columns
@@ -296,7 +341,16 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
     // per warp, not per row.
     auto step = [&](int t, int u, auto edge_tag) {
         constexpr bool EDGE = decltype(edge_tag)::value;
-        consume((unsigned)(t + 2 * R), wl[0][(u + 2 * R) % NW]);
+        {
+            const unsigned r = (unsigned)(t + 2 * R);
+            if constexpr (CT) {
+                // t = it * S + u: slot (u + 2R) mod S and phase are known per u
+                consume(r, (unsigned)((u + 2 * R) % S), (par_it ^ (unsigned)(((u + 2 * R) / S) & 1)),
+                        wl[0][(u + 2 * R) % NW]);
+            } else {
+                consume(r, r % S, (r / S) & 1u, wl[0][(u + 2 * R) % NW]);
+            }
+        }
         const int y1 = ys - (NSW - 1) * R + t;
 #pragma unroll
         for (int k = 1; k <= NSW; ++k) {
@@ -314,7 +368,7 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
 #pragma unroll
                     for (int p = 0; p < V; ++p) {               // boundary ring: held value
                         if (!(yint && xin[p]))
-                            v[p] = IsSep<Op>::value ? ring[((unsigned)(yk - row0) & (S - 1)) * WS + lo_e + p]
+                            v[p] = IsSep<Op>::value ? ring[((unsigned)(yk - row0) % S) * WS + lo_e + p]
                                                     : wl[k - 1][(ph + R) % NW][R + p];
                     }
                 }
@@ -335,16 +389,16 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
     };
 
 #pragma unroll
-    for (int r = 0; r < 2 * R; ++r) consume((unsigned)r, wl[0][r]);
-    const int nt = ye - ys + 2 * (NSW - 1) * R;            // sweep-1 rows
+    for (int r = 0; r < 2 * R; ++r) consume((unsigned)r, (unsigned)r, 0u, wl[0][r]);
     auto march = [&](auto edge_tag) {
         int t = 0;
-        for (; t + NW <= nt; t += NW) {
+        constexpr int UN = CT ? S : NW;                    // steps per unrolled body
+        for (; t + UN <= nt; t += UN, par_it ^= 1u) {
 #pragma unroll
-            for (int u = 0; u < NW; ++u) step(t + u, u, edge_tag);
+            for (int u = 0; u < UN; ++u) step(t + u, u, edge_tag);
         }
 #pragma unroll
-        for (int u = 0; u < NW - 1; ++u)
+        for (int u = 0; u < UN - 1; ++u)
             if (t + u < nt) step(t + u, u, edge_tag);
     };
     bool all_x = true;
