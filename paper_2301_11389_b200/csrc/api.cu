@@ -183,7 +183,7 @@ extern "C" int stencil_create(stencil_t* out, int kind, int ndims, const int64_t
 // Gpt/s SHUFFLE vs PLAIN).  Within 2% either way: SHUFFLE (the paper's form).
 static int auto_variant(const stencil_s* h) {
     switch (h->k->kind) {
-    case ST_GAUSSBLUR5X5:  // 8192^2 two sweeps per pass: 1363 vs 1392
+    case ST_GAUSSBLUR5X5:  // 8192^2 two sweeps per pass: 1380 vs 1398
     case ST_GAMEOFLIFE:    // 16384^2 packed three-sweep: 1858 vs 1889
     case ST_WAVE13PT:      // fp64 512^3: 250 vs 257
     case ST_JACOBI3D7:     // fp32 1024^3: 697 vs 710
