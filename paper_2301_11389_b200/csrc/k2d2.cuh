@@ -61,6 +61,9 @@ template <int R, typename T> constexpr int k2d2_stages() {
     return k2d2_ct<R, T>() ? (R == 1 ? 12 : STB200_2D2_S2) : kStages2D2;
 }
 template <int NW> __host__ __device__ constexpr int k2d2_threads() { return (NW + 1) * 32; }
+#ifndef STB200_2D2_BACKOFF
+#define STB200_2D2_BACKOFF 512    // producer: longest nanosleep between polls of a busy stage
+#endif
 #ifndef STB200_2D2_FBSEL
 #define STB200_2D2_FBSEL 1        // SHUFFLE fallback as one load + selects (0: predicated asm loads)
 #endif
@@ -161,7 +164,7 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
             T* dst0 = ring + (g_lo - (X0 - NSW * V));
             unsigned s = 0, ph = 0;                        // slot of row r, phase of its (r / S)-th use
             for (int r = 0; r < nrows; ++r, s = s + 1 == S ? (ph ^= 1u, 0u) : s + 1) {
-                if (r >= S) mbar_wait_backoff<512>(&empty[s], ph ^ 1u);
+                if (r >= S) mbar_wait_backoff<STB200_2D2_BACKOFF>(&empty[s], ph ^ 1u);
                 const int yin = row0 + r;
                 if (yin >= 0 && yin < ny) {
                     mbar_arrive_expect_tx(&full[s], bytes);
