@@ -74,3 +74,32 @@ def test_slab_plan_is_exported_host_logic(L):
     from paper_2301_11389_b200 import binding
     p = binding.slab_plan(16, 1, 1, 0, 2)
     assert p["own_end"] - p["own_begin"] == 8
+
+
+def _header_enum(name):
+    """{enumerator: value} of `enum <name> { ... };` in include/stencil.h."""
+    src = open(os.path.join(ROOT, "include", "stencil.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    body = re.search(r"enum\s+" + name + r"\s*\{(.*?)\};", src, flags=re.S).group(1)
+    out, nxt = {}, 0
+    for item in (t.strip() for t in body.split(",")):
+        if not item:
+            continue
+        k, _, v = item.partition("=")
+        nxt = int(v.strip(), 0) if v.strip() else nxt
+        out[k.strip()] = nxt
+        nxt += 1
+    return out
+
+
+def test_binding_constants_match_the_header():
+    """The binding's name -> value maps are the header's enums (kinds,
+    dtypes, variants incl. ST_AUTO): argument marshalling only, no drift."""
+    from paper_2301_11389_b200 import binding
+    kinds = _header_enum("stencil_kind")
+    assert {("ST_" + k.upper()): v for k, v in binding.KINDS.items()} == kinds
+    dtypes = _header_enum("stencil_dtype")
+    assert {("ST_" + k.upper()): v for k, v in binding.DTYPES.items()} == dtypes
+    variants = _header_enum("stencil_variant")
+    assert {("ST_" + k.upper()): v for k, v in binding.VARIANTS.items()} == variants
+    assert variants["ST_AUTO"] == binding.VARIANTS["auto"]
