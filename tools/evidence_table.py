@@ -20,10 +20,11 @@ PTS = {"gaussblur": 8188 ** 2, "jacobi2d_paper": 32766 ** 2, "gameoflife": 16382
        "laplacian": 510 ** 3, "wave13pt": 508 ** 3, "jacobi3d": 1022 ** 3, "divergence": 510 ** 3,
        "gradient": 510 ** 3, "tricubic": 253 ** 3,
        # two-sweep (k2d2) launches: one read and one write per launch, 2 sweeps
-       "jacobi2d_pair": 32766 ** 2, "gameoflife_pair": 16382 ** 2}
+       "jacobi2d_pair": 32766 ** 2, "gameoflife_pair": 16382 ** 2,
+       "jacobi2d_paper_pair": 32766 ** 2, "gaussblur_pair": 8188 ** 2}
 BPP = {"gaussblur": 8, "jacobi2d_paper": 8, "gameoflife": 8, "laplacian": 16, "wave13pt": 24,
        "jacobi3d": 8, "divergence": 16, "gradient": 16, "tricubic": 20, "jacobi2d_pair": 8,
-       "gameoflife_pair": 8}
+       "gameoflife_pair": 8, "jacobi2d_paper_pair": 8, "gaussblur_pair": 8}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 TSCALE = {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
 
