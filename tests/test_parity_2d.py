@@ -196,3 +196,35 @@ def test_gaussblur_8192_x100_runs_repeat_bit_identically():
             ref = bufs[idx]
         else:
             assert torch.equal(bufs[idx], ref), f"{var}: run differs from the first run"
+
+
+@pytest.mark.parametrize("kind,dtype,fusion", [
+    ("gaussblur5x5", "f32", 2), ("jacobi2d5", "f32", 3), ("jacobi2d5", "f32", 2), ("jacobi2d9", "f32", 2),
+    ("jacobi2d9", "f64", 2), ("gameoflife", "i32", 3)])
+@pytest.mark.parametrize("ny", [1000, 1507, 2231])
+@pytest.mark.parametrize("variant", ["shuffle", "plain"])
+def test_streaming_strips_every_tail(oracle, kind, dtype, fusion, ny, variant):
+    """Grids tall enough that the streaming kernels' strips run the unrolled
+    march body (one ring pass per S steps, S = 10 / 12 compile-time ring
+    slots) and then tails of different lengths: strips of
+    6-15 rows with 2-4 extra halo rows give sweep-row counts of every residue
+    mod S across these heights.  Bit-identical to single sweeps, oracle parity."""
+    import torch
+    from paper_2301_11389_b200.binding import Stencil
+    shape = (ny, 1028)
+    f = inputs.generate_np(shape, dtype, inputs.BASE_SEED + 21)
+    n = 6
+    bufs = [f.copy(), np.zeros_like(f)]
+    ridx = oracle.run(kind, dtype, bufs, n)
+    res = {}
+    for fu in (1, fusion):
+        st = Stencil(kind, shape[::-1], dtype, variant=variant)
+        st.set_fusion(fu)
+        d = [torch.from_numpy(f.copy()).cuda(), torch.zeros(shape, dtype=torch.from_numpy(f).dtype,
+                                                           device="cuda")]
+        idx = st.run(d, n)
+        torch.cuda.synchronize()
+        res[fu] = d[idx].cpu().numpy()
+        st.close()
+    assert np.array_equal(res[1].view(np.uint8), res[fusion].view(np.uint8)), "fused != single sweeps"
+    assert_parity(res[fusion], bufs[ridx], dtype, f"{kind} {dtype} ny={ny} fusion={fusion} {variant}")
