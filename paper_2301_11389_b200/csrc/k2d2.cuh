@@ -51,6 +51,9 @@ constexpr int kStages2D2 = STB200_2D2_S;
 #ifndef STB200_2D2_S2
 #define STB200_2D2_S2 10          // CT ring stages for radius 2 (a multiple of 5)
 #endif
+#ifndef STB200_2D2_RBS
+#define STB200_2D2_RBS 2          // CT: SHUFFLE release batch (2: gaussblur 1378 -> 1391, Jacobi even)
+#endif
 #ifndef STB200_2D2_RBP
 #define STB200_2D2_RBP 0          // CT: PLAIN release batch (0: 4 if it divides S, else 2)
 #endif
@@ -207,7 +210,7 @@ k2d2(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int ny, int y_lo
     const uint32_t rt_zero = (uint32_t)((uint64_t)nx >> 48);   // 0 at run time, unknown to the compiler
     // rows released per fence (pipe.cuh ring_release_lagged): 4 for PLAIN,
     // 1 for SHUFFLE; with compile-time slots a divisor of S
-    constexpr unsigned RB = VARIANT == VAR_PLAIN ? (STB200_2D2_RBP ? STB200_2D2_RBP : S % 4 == 0 ? 4 : 2) : 1;
+    constexpr unsigned RB = VARIANT == VAR_PLAIN ? (STB200_2D2_RBP ? STB200_2D2_RBP : S % 4 == 0 ? 4 : 2) : (CT ? STB200_2D2_RBS : 1);
     static_assert(!CT || S % RB == 0, "release batch divides the ring");
     // consume input row r from ring slot s (= r mod S) whose fill phase is par
     auto consume = [&](unsigned r, unsigned s, unsigned par, T* dst) {
