@@ -100,12 +100,12 @@ def test_graph_cache_and_variant_switch(oracle):
 
 
 @pytest.mark.parametrize("kind,dtype,expect", [
-    ("gaussblur5x5", "f32", "plain"), ("jacobi2d5", "f32", "shuffle"), ("tricubic", "f32", "plain"),
-    ("lapgsrb", "f32", "shuffle"), ("gameoflife", "i32", "plain")])
+    ("gaussblur5x5", "f32", "shuffle"), ("jacobi2d5", "f32", "shuffle"), ("tricubic", "f32", "plain"),
+    ("lapgsrb", "f32", "shuffle"), ("gameoflife", "i32", "shuffle"), ("wave13pt", "f64", "plain")])
 def test_auto_variant_resolves_per_kind(kind, dtype, expect):
     """ST_AUTO resolves in the library to the kind's measured-faster variant
     (stencil.h) and stencil_get_variant reports it."""
-    shape = (12, 12, 132) if kind in ("tricubic", "lapgsrb") else (40, 136)
+    shape = (12, 12, 132) if kind in ("tricubic", "lapgsrb", "wave13pt") else (40, 136)
     st = Stencil(kind, shape[::-1], dtype, variant="auto")
     assert st.variant == expect
     assert st.info()["variant"] == (0 if expect == "shuffle" else 1)
